@@ -1,0 +1,183 @@
+/*
+ * mp.h -- C ABI of the B200-native PTD-P hot path (arXiv 2104.04473).
+ *
+ * Narayanan et al., "Efficient Large-Scale Language Model Training on GPU
+ * Clusters Using Megatron-LM" (SC'21).  Citations: P:n = PAPER.md line n.
+ *
+ * The library computes the forward and backward of GPT transformer layers
+ * under Megatron tensor parallelism (Sec. 2.3: column-parallel
+ * QKV/FC1, row-parallel projection/FC2, conjugate f/g operators) composed with
+ * the pipeline schedules of Sec. 2.2 (GPipe P:104-107, 1F1B P:109,
+ * interleaved 1F1B P:112-120), with one process per GPU and NCCL for the
+ * tensor-parallel all-reduces and pipeline point-to-point transfers.
+ *
+ * Conventions
+ *  - Every call returns an mp_status; no exceptions or exit() cross the ABI.
+ *    mp_last_error() gives a thread-local message for the last failure.
+ *  - Indices are 0-based (the paper's figures number microbatches from 1).
+ *  - Caller-owned buffers are borrowed for the duration of the call; device
+ *    buffers passed to *_fwd/*_bwd calls are used in stream order on the
+ *    given CUDA stream (cudaStream_t passed as void*; NULL = legacy stream).
+ *  - The library owns weights, gradients, optimizer state, activation stash,
+ *    NCCL communicators and internal streams; mp_finalize releases them.
+ *  - There is no CPU fallback: compute calls fail with MP_ECUDA when no
+ *    sm_100 device is present.  Host-only calls (mp_flops, mp_param_count,
+ *    mp_get_schedule, mp_get_stage_map, mp_validate) need no GPU.
+ */
+#ifndef MP_H_
+#define MP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  MP_OK = 0,
+  MP_EINVAL = 1,        /* bad argument (null pointer, out-of-range index, unknown name) */
+  MP_EDIV = 2,          /* divisibility violated: h%a, a%t, 4h%t, V%t, l%(p*v), t*p*d != world */
+  MP_EBUDGET = 3,       /* device memory budget exceeded (S:175 BudgetError) */
+  MP_ESCHED = 4,        /* schedule invalid: interleaved needs m % p == 0; v > 1 only for interleaved */
+  MP_ENOMEM = 5,        /* allocation failed */
+  MP_ECUDA = 6,         /* CUDA error or no usable sm_100 device */
+  MP_ENCCL = 7,         /* NCCL error */
+  MP_ESTATE = 8,        /* call order (e.g. layer call before mp_set_weights) */
+  MP_EUNSUPPORTED = 9   /* valid in the paper but not built here (e.g. d > 1) */
+} mp_status;
+
+typedef enum { MP_GPIPE = 0, MP_1F1B = 1, MP_INTERLEAVED = 2 } mp_schedule;
+typedef enum { MP_FP32 = 0, MP_BF16 = 1 } mp_dtype;
+
+/* GPT model shape (V = 51200, s = 2048 in the paper's models). */
+typedef struct {
+  int l;                 /* transformer layers */
+  int h;                 /* hidden size */
+  int a;                 /* attention heads */
+  int s;                 /* sequence length */
+  int V;                 /* vocabulary size */
+  mp_dtype dtype;        /* storage/compute precision of the path (fp32 math inside bf16 kernels) */
+  float p_drop_attn;     /* attention-probability dropout (reading #7); 0 = off */
+  float p_drop_hidden;   /* hidden dropout after proj / FC2; 0 = off */
+  float ln_eps;          /* LayerNorm epsilon (reading #2: 1e-5) */
+  int recompute;         /* activation recomputation; counted by mp_flops only in round 1 */
+  unsigned long long seed;  /* dropout stream key */
+  float lr;              /* Adam learning rate for mp_run_batch(apply_optimizer=1) */
+} mp_model_cfg;
+
+/* Per-batch statistics filled by mp_run_batch. */
+typedef struct {
+  double iter_seconds;          /* device time of the batch on this rank (events around the whole batch) */
+  double model_flops;           /* Eq. (2) F for this batch (72-variant without recompute) */
+  double model_tflops_per_gpu;  /* F / (n * iter_seconds) / 1e12 */
+  double busy_seconds;          /* sum of this rank's task durations (forward/backward chunk work) */
+  double bubble_measured;       /* (iter_seconds - busy)/busy on this rank */
+  double bubble_formula;        /* (p-1)/m or (p-1)/(v m) */
+  int peak_inflight;            /* max stashed (microbatch, chunk) on this rank */
+  int n_tasks;                  /* tasks executed on this rank (2 m v) */
+} mp_batch_stats;
+
+typedef struct mp_ctx mp_ctx;   /* opaque; one per process (= one GPU) */
+
+/* ---------------------------------------------------------------- host-only */
+
+/* Eq. (2): F = 96 B s l h^2 (1 + s/(6h) + V/(16 l h)) when
+ * recompute != 0; otherwise 72 B s l h^2 (1 + s/(6h)) + 6 B s h V. */
+double mp_flops(long long B, long long s, long long l, long long h, long long V, int recompute);
+
+/* Eq. (1) as the exact integer 12 l h^2 + 13 l h + (V + s) h. */
+unsigned long long mp_param_count(long long l, long long h, long long s, long long V);
+
+/* Validate a parallel configuration: returns MP_OK, MP_EDIV,
+ * MP_ESCHED or MP_EUNSUPPORTED.  m = B/(b d) is checked when B > 0. */
+mp_status mp_validate(const mp_model_cfg* cfg, int t, int p, int v, int d, int B, int b,
+                      mp_schedule sched);
+
+/* Per-device task order of a schedule.  `triples` receives
+ * 3 * 2*m*v ints: (kind 0 = forward / 1 = backward, microbatch, chunk) in
+ * execution order for device `device` in [0, p); *n receives the number of
+ * tasks.  `triples` may be NULL to query *n only.  Errors: MP_ESCHED
+ * (m % p != 0 for interleaved; v != 1 for GPipe/1F1B), MP_EINVAL. */
+mp_status mp_get_schedule(int p, int m, int v, mp_schedule sched, int device, int* triples, int* n);
+
+/* Layer -> (device, chunk) map: stage sigma = chunk * p + device
+ * owns layers [sigma L_c, (sigma+1) L_c), L_c = l / (p v).  Output arrays
+ * have l entries.  MP_EDIV if l % (p v) != 0. */
+mp_status mp_get_stage_map(int l, int p, int v, int* dev_of_layer, int* chunk_of_layer);
+
+/* Thread-local description of the last error. */
+const char* mp_last_error(void);
+
+/* Size of the NCCL unique id blob mp_init expects (NCCL_UNIQUE_ID_BYTES). */
+int mp_nccl_id_bytes(void);
+/* Create a new NCCL unique id into `out` (mp_nccl_id_bytes() bytes); rank 0
+ * calls this and the launcher broadcasts the bytes to every rank. */
+mp_status mp_nccl_get_id(void* out);
+
+/* ---------------------------------------------------------------- context */
+
+/* Collective over n = t*p*d ranks.  Ranks are laid out with
+ * tensor parallelism fastest: world_rank = (dp * p + pp) * t + tp.
+ * `nccl_id` is the world communicator id from mp_nccl_get_id on rank 0.
+ * Validates divisibility (MP_EDIV), sets the CUDA device to local_device,
+ * builds the TP communicator, the four directed pipeline channels per rank
+ * (activations to / from the neighbours, gradients to / from) and the
+ * tied-embedding communicator, allocates this rank's weight shards (bf16 or
+ * fp32), fp32 gradient accumulators and fp32 Adam state.  d > 1 returns
+ * MP_EUNSUPPORTED in this round. */
+mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world_rank, int world_size,
+                  int local_device, const void* nccl_id, mp_ctx** out);
+mp_status mp_finalize(mp_ctx* ctx);
+
+/* Weights in the UNPARTITIONED layout of gen/__init__.py, host fp32, row-major,
+ * math orientation Y = X W (W_qkv [h, 3h] head-major columns, W_o [h, h],
+ * W_1 [h, 4h], W_2 [4h, h]; vectors [n]).  Names: ln1_g ln1_b w_qkv b_qkv w_o
+ * b_o ln2_g ln2_b w_1 b_1 w_2 b_2 (per layer, `layer` in [0, l)), and emb
+ * pos lnf_g lnf_b (layer ignored).  The library keeps only this rank's shard
+ * if this rank owns the layer (MP_OK and no-op otherwise).
+ * Values are rounded to the storage dtype. */
+mp_status mp_set_weights(mp_ctx* ctx, const char* name, int layer, const float* host);
+/* Read back this rank's shard of a weight / fp32 gradient accumulator into
+ * host fp32 memory, in the shard's math orientation (e.g. W_qkv[:, cols of
+ * this rank's heads]).  *n receives the element count; host may be NULL to
+ * query the size.  MP_EINVAL if this rank does not own the layer. */
+mp_status mp_get_weights(mp_ctx* ctx, const char* name, int layer, float* host, long long* n);
+mp_status mp_get_grads(mp_ctx* ctx, const char* name, int layer, float* host, long long* n);
+/* Zero all gradient accumulators. */
+mp_status mp_zero_grads(mp_ctx* ctx);
+
+/* ----------------------------------------------------------- layer calls */
+
+/* One transformer layer forward on this rank's TP group (collective over the
+ * t ranks that share the stage): x, y device [s, b, h] in the storage dtype
+ * (the paper's [s, b, a, h] layout).  The activations needed by the
+ * backward are stashed in a library-owned slot returned in *stash_slot.
+ * Runs on `stream`. */
+mp_status mp_layer_fwd(mp_ctx* ctx, int layer, int b, const void* x, void* y, int* stash_slot,
+                       void* stream);
+/* Backward of a stashed forward: dy -> dx (device [s, b, h]); weight
+ * gradients are accumulated (fp32) into the library's accumulators; the
+ * stash slot is released.  Collective over the TP group. */
+mp_status mp_layer_bwd(mp_ctx* ctx, int layer, int b, int stash_slot, const void* dy, void* dx,
+                       void* stream);
+
+/* ------------------------------------------------------------- batch call */
+
+/* One training iteration of B sequences under `sched`:
+ * m = B/(b d) microbatches of b sequences; tokens host int32 [B, s+1]
+ * (inputs tok[:, :s], labels tok[:, 1:]); every rank passes the same tokens.
+ * Executes this rank's static task order (mp_get_schedule) with P2P
+ * transfers on FIFO channels, flushes, all-reduces the tied
+ * embedding gradient between the first and last stage, and, if
+ * apply_optimizer, runs one Adam step (lr from cfg) on every parameter.
+ * Gradients are zeroed at the start of the batch.  *loss_out = mean token
+ * cross-entropy over the B*s tokens (same value on every rank).  stats may
+ * be NULL.  Collective over all ranks. */
+mp_status mp_run_batch(mp_ctx* ctx, int B, int b, int m, mp_schedule sched, const int* tokens,
+                       int apply_optimizer, float* loss_out, mp_batch_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MP_H_ */

@@ -1,0 +1,438 @@
+// Batched GEMM engine of the hot path (SURVEY 8(a) rows a6, a7, a9, a10,
+// a14, a16, a17, a18): C_z (+)= alpha * A_z B_z + bias.
+//
+// bf16: persistent, warp-specialised tcgen05 kernel for sm_100a.
+//   warp 0  : TMA producer (one elected lane), 128B-swizzled tiles into a
+//             STAGES-deep shared-memory ring guarded by full/empty mbarriers;
+//   warp 1  : TMEM allocator + MMA issuer (one lane issues tcgen05.mma
+//             128 x BN x 16, fp32 accumulators in TMEM, double buffered so
+//             the epilogue of tile i overlaps the main loop of tile i+1);
+//   warps 2-5: epilogue, tcgen05.ld 32 columns per thread (one TMEM lane =
+//             one output row), + bias, convert, vectorised global stores or
+//             fp32 read-modify-write accumulation (weight gradients).
+// Operands may be K-major or MN-major (the dX and dW GEMMs of the backward
+// and the P V / P^T dO attention products read MN-major tiles directly, so
+// no transpose is ever materialised -- the point of the paper's [s,b,a,h]
+// layout).
+// fp32: a plain SIMT FFMA tiled kernel with the same semantics (parity mode).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "ptx.cuh"
+#include "common.h"
+#include "../../include/mp_ops.h"
+
+namespace mp {
+
+constexpr int BM = 128;
+constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
+constexpr int EPI_WARPS = 4;
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
+
+template <int BN>
+struct TcCfg {
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = 2 * BN;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+struct TcArgs {
+  int M, N, K, batch;
+  int m_blocks, n_blocks, num_tiles;
+  void* C;
+  long long ldc, strideC;
+  const __nv_bfloat16* bias;
+  int c_fp32, accumulate, causal, vec_ok;
+  float alpha;
+};
+
+__device__ __forceinline__ bool tile_skipped(const TcArgs& g, int m_blk, int n_blk, int BN) {
+  return g.causal == 1 && n_blk * BN > m_blk * BM + BM - 1;
+}
+__device__ __forceinline__ void k_range(const TcArgs& g, int m_blk, int& kb0, int& kb1) {
+  int kend = g.K;
+  kb0 = 0;
+  if (g.causal == 2) kend = min(g.K, (m_blk + 1) * BM);
+  if (g.causal == 3) kb0 = (m_blk * BM) / BK;
+  kb1 = (kend + BK - 1) / BK;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs g) {
+  using Cfg = TcCfg<BN>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
+  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  const int tiles_per_batch = g.m_blocks * g.n_blocks;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------ TMA producer
+      int stage = 0; uint32_t phase = 0;
+      for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
+        const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
+        const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+        if (tile_skipped(g, m_blk, n_blk, BN)) continue;
+        int kb0, kb1; k_range(g, m_blk, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          uint8_t* a = sA + stage * Cfg::A_BYTES;
+          uint8_t* b = sB + stage * Cfg::B_BYTES;
+          if (!A_MN) {
+            tma_load_3d(a, &tmA, &full[stage], kb * BK, m_blk * BM, z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_3d(a + j * 8192, &tmA, &full[stage], m_blk * BM + 64 * j, kb * BK, z);
+          }
+          if (!B_MN) {
+            tma_load_3d(b, &tmB, &full[stage], kb * BK, n_blk * BN, z);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 64; ++j)
+              tma_load_3d(b + j * 8192, &tmB, &full[stage], n_blk * BN + 64 * j, kb * BK, z);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------ MMA issuer
+      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+      int stage = 0; uint32_t phase = 0;
+      int acc = 0; uint32_t acc_phase = 0;
+      for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
+        const int rem = t % tiles_per_batch;
+        const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+        if (tile_skipped(g, m_blk, n_blk, BN)) continue;
+        int kb0, kb1; k_range(g, m_blk, kb0, kb1);
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * Cfg::A_BYTES);
+          const uint32_t b_addr = smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major SW128: rows of 128 B, 8-row atoms 1024 B apart (SBO);
+            //   the k-th 16-wide slice starts 32 B further into the row.
+            // MN-major SW128: 64-element MN blocks 8 KB apart (LBO), 8-row
+            //   K groups 1024 B apart (SBO); the k-th slice is 16 rows = 2 KB on.
+            const uint64_t ad = A_MN ? smem_desc_sw128(a_addr + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(a_addr + k * 32, 16, 1024);
+            const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + k * 2048, 8192, 1024)
+                                     : smem_desc_sw128(b_addr + k * 32, 16, 1024);
+            umma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // -------------------------------------------------- epilogue
+    const int quarter = warp % 4;            // TMEM lanes 32*quarter .. +31
+    int acc = 0; uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
+      const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
+      const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+      if (tile_skipped(g, m_blk, n_blk, BN)) continue;
+      int kb0, kb1; k_range(g, m_blk, kb0, kb1);
+      const bool have_acc = kb1 > kb0;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const int row = m_blk * BM + quarter * 32 + lane;
+      const bool row_ok = row < g.M;
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        const int col0 = n_blk * BN + c0;
+        if (col0 >= g.N) break;
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(quarter * 32) << 16), r);
+        tmem_ld_wait();
+        if (!row_ok) continue;
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = have_acc ? __uint_as_float(r[j]) * g.alpha : 0.f;
+        const int ncols = min(32, g.N - col0);
+        if (g.bias) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (j < ncols) v[j] += __bfloat162float(g.bias[col0 + j]);
+        }
+        const long long off = (long long)z * g.strideC + (long long)row * g.ldc + col0;
+        if (g.c_fp32) {
+          float* C = reinterpret_cast<float*>(g.C) + off;
+          if (g.vec_ok && ncols == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+              if (g.accumulate) {
+                float4 c = *reinterpret_cast<const float4*>(C + j);
+                o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+              }
+              *reinterpret_cast<float4*>(C + j) = o;
+            }
+          } else {
+            for (int j = 0; j < ncols; ++j) C[j] = g.accumulate ? C[j] + v[j] : v[j];
+          }
+        } else {
+          __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(g.C) + off;
+          if (g.vec_ok && ncols == 32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              uint4 o;
+              __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j], v[j + 1]);
+              __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+              __nv_bfloat162 p2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
+              __nv_bfloat162 p3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+              o.x = *reinterpret_cast<uint32_t*>(&p0);
+              o.y = *reinterpret_cast<uint32_t*>(&p1);
+              o.z = *reinterpret_cast<uint32_t*>(&p2);
+              o.w = *reinterpret_cast<uint32_t*>(&p3);
+              *reinterpret_cast<uint4*>(C + j) = o;
+            }
+          } else {
+            for (int j = 0; j < ncols; ++j) C[j] = __float2bfloat16_rn(v[j]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+}
+
+// ----------------------------------------------------------- fp32 SIMT GEMM
+constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
+
+__global__ void __launch_bounds__(256)
+simt_gemm_kernel(mp_gemm_desc g, int m_blocks, int n_blocks) {
+  __shared__ float As[SB_K][SB_M + 4];
+  __shared__ float Bs[SB_K][SB_N + 4];
+  const int z = blockIdx.z;
+  const int m_blk = blockIdx.x, n_blk = blockIdx.y;
+  const int m0 = m_blk * SB_M, n0 = n_blk * SB_N;
+  if (g.causal == 1 && n0 > m0 + SB_M - 1) return;
+  int k0 = 0, k1 = g.K;
+  if (g.causal == 2) k1 = min(g.K, (m0 / BM + 1) * BM);
+  if (g.causal == 3) k0 = (m0 / BM) * BM;
+  const float* A = reinterpret_cast<const float*>(g.A) + (long long)z * g.strideA;
+  const float* B = reinterpret_cast<const float*>(g.B) + (long long)z * g.strideB;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4] = {};
+  for (int kk = k0; kk < k1; kk += SB_K) {
+    for (int i = threadIdx.x; i < SB_K * SB_M; i += 256) {
+      int kq = i / SB_M, mq = i % SB_M;          // mq fastest: coalesced for MN-major
+      int m = m0 + mq, k = kk + kq;
+      float va = 0.f;
+      if (m < g.M && k < k1) va = g.a_major ? A[(long long)k * g.lda + m] : A[(long long)m * g.lda + k];
+      As[kq][mq] = va;
+      int n = n0 + mq;
+      float vb = 0.f;
+      if (n < g.N && k < k1) vb = g.b_major ? B[(long long)k * g.ldb + n] : B[(long long)n * g.ldb + k];
+      Bs[kq][mq] = vb;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kq = 0; kq < SB_K; ++kq) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) { a[i] = As[kq][ty * 4 + i]; b[i] = Bs[kq][tx * 4 + i]; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* C = reinterpret_cast<float*>(g.C) + (long long)z * g.strideC;
+  const float* bias = reinterpret_cast<const float*>(g.bias);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n >= g.N) continue;
+      float v = acc[i][j] * g.alpha + (bias ? bias[n] : 0.f);
+      float* c = C + (long long)m * g.ldc + n;
+      *c = g.accumulate ? *c + v : v;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 3-D bf16 tensor map: dims (inner, outer, batch), 128B swizzle, box (64, box_outer, 1).
+static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t batch,
+                     uint64_t ld_elems, uint64_t batch_stride_elems, uint32_t box_outer) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  if (batch <= 1) { batch = 1; batch_stride_elems = ld_elems * outer; }
+  cuuint64_t dims[3] = {inner, outer, batch};
+  cuuint64_t strides[2] = {ld_elems * 2, batch_stride_elems * 2};
+  cuuint32_t box[3] = {64, box_outer, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int pick_bn(const mp_gemm_desc& g) {
+  if (g.N <= 64) return 64;
+  if (g.N <= 128) return 128;
+  // prefer 256-wide tiles unless that leaves most SMs idle
+  long long tiles256 = (long long)((g.M + BM - 1) / BM) * ((g.N + 255) / 256) * g.batch;
+  if (tiles256 < num_sms() / 2) return 128;
+  return 256;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcArgs& a, int grid,
+                             cudaStream_t st) {
+  using Cfg = TcCfg<BN>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, a);
+  return cudaGetLastError();
+}
+
+template <int BN>
+static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, const TcArgs& a, int grid,
+                                  int am, int bm, cudaStream_t st) {
+  if (!am && !bm) return launch_tc<BN, false, false>(ta, tb, a, grid, st);
+  if (!am && bm) return launch_tc<BN, false, true>(ta, tb, a, grid, st);
+  if (am && !bm) return launch_tc<BN, true, false>(ta, tb, a, grid, st);
+  return launch_tc<BN, true, true>(ta, tb, a, grid, st);
+}
+
+static int tc_grid(const TcArgs& a) { return std::max(1, std::min(a.num_tiles, num_sms())); }
+
+mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return set_err(MP_EINVAL, "gemm: empty shape");
+  if (g.accumulate && !g.c_fp32) return set_err(MP_EINVAL, "gemm: accumulate needs fp32 C");
+  auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (!al16(g.A) || !al16(g.B) || (g.lda * 2) % 16 || (g.ldb * 2) % 16 || (g.strideA * 2) % 16 ||
+      (g.strideB * 2) % 16)
+    return set_err(MP_EINVAL, "gemm: TMA needs 16-byte aligned operands and strides");
+  const int BN = pick_bn(g);
+  CUtensorMap ta, tb;
+  bool ok = g.a_major ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.strideA, BK)
+                      : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.strideA, BM);
+  ok = ok && (g.b_major ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.strideB, BK)
+                        : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.strideB, BN));
+  if (!ok) return set_err(MP_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
+  TcArgs a;
+  a.M = g.M; a.N = g.N; a.K = g.K; a.batch = g.batch;
+  a.m_blocks = (g.M + BM - 1) / BM;
+  a.n_blocks = (g.N + BN - 1) / BN;
+  a.num_tiles = a.m_blocks * a.n_blocks * g.batch;
+  a.C = g.C; a.ldc = g.ldc; a.strideC = g.strideC;
+  a.bias = reinterpret_cast<const __nv_bfloat16*>(g.bias);
+  a.c_fp32 = g.c_fp32; a.accumulate = g.accumulate; a.causal = g.causal; a.alpha = g.alpha;
+  const int esz = g.c_fp32 ? 4 : 2;
+  a.vec_ok = al16(g.C) && (g.ldc * esz) % 16 == 0 && (g.strideC * esz) % 16 == 0;
+  const int grid = tc_grid(a);
+  cudaError_t e;
+  if (BN == 64) e = dispatch_major<64>(ta, tb, a, grid, g.a_major, g.b_major, st);
+  else if (BN == 128) e = dispatch_major<128>(ta, tb, a, grid, g.a_major, g.b_major, st);
+  else e = dispatch_major<256>(ta, tb, a, grid, g.a_major, g.b_major, st);
+  if (e != cudaSuccess) return set_err(MP_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
+  return MP_OK;
+}
+
+mp_status gemm_fp32(const mp_gemm_desc& g, cudaStream_t st) {
+  if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return set_err(MP_EINVAL, "gemm: empty shape");
+  dim3 grid((g.M + SB_M - 1) / SB_M, (g.N + SB_N - 1) / SB_N, g.batch);
+  simt_gemm_kernel<<<grid, 256, 0, st>>>(g, grid.x, grid.y);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(MP_ECUDA, "simt gemm launch: %s", cudaGetErrorString(e));
+  return MP_OK;
+}
+
+mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st) {
+  return dt == MP_BF16 ? gemm_bf16(g, st) : gemm_fp32(g, st);
+}
+
+}  // namespace mp
+
+extern "C" mp_status mp_op_gemm(mp_dtype dtype, const mp_gemm_desc* g, void* stream) {
+  if (!g) return mp::set_err(MP_EINVAL, "null desc");
+  MP_REQUIRE_DEVICE();
+  return mp::gemm(dtype, *g, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" mp_status mp_op_gemm_config(const mp_gemm_desc* g, int* out3) {
+  if (!g || !out3) return mp::set_err(MP_EINVAL, "null arg");
+  MP_REQUIRE_DEVICE();
+  int BN = mp::pick_bn(*g);
+  out3[0] = BN;
+  out3[1] = BN == 256 ? mp::TcCfg<256>::STAGES : (BN == 128 ? mp::TcCfg<128>::STAGES : mp::TcCfg<64>::STAGES);
+  long long tiles = (long long)((g->M + mp::BM - 1) / mp::BM) * ((g->N + BN - 1) / BN) * g->batch;
+  out3[2] = (int)std::max(1LL, std::min<long long>(tiles, mp::num_sms()));
+  return MP_OK;
+}
