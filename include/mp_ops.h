@@ -59,6 +59,45 @@ mp_status mp_op_gemm(mp_dtype dtype, const mp_gemm_desc* g, void* stream);
  * out[0] = BN, out[1] = stages, out[2] = grid size. */
 mp_status mp_op_gemm_config(const mp_gemm_desc* g, int* out3);
 
+/* LayerNorm over rows of x [R, h] (implied by Eq. (1)'s 13h term, P:344;
+ * pre-LN GPT layer, reading #1; biased variance, eps): y = g * xhat + b;
+ * per-row fp32 mean / rstd saved for the backward.  h <= 8192 (bf16). */
+mp_status mp_op_layernorm_fwd(mp_dtype dt, const void* x, const void* g, const void* b, void* y, float* mean,
+                              float* rstd, int R, int h, float eps, void* stream);
+
+/* Fused bias-dropout-add + LayerNorm (P:312 fusion; dropout p = 0 here):
+ * x1 = r + (y + bias) (stored), out = LN(x1; g, b). */
+mp_status mp_op_bda_layernorm_fwd(mp_dtype dt, const void* y, const void* bias, const void* r, void* x1,
+                                  const void* g, const void* b, void* out, float* mean, float* rstd, int R, int h,
+                                  float eps, void* stream);
+
+/* LayerNorm backward: dx = LN'(dy) (+ dres if non-NULL); dgamma, dbeta
+ * (fp32 [h]) are ACCUMULATED (+=).  scratch: fp32 workspace of
+ * mp_op_layernorm_bwd_scratch_floats(R, h) floats. */
+mp_status mp_op_layernorm_bwd(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
+                              const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
+                              float* scratch, int R, int h, void* stream);
+long long mp_op_layernorm_bwd_scratch_floats(int R, int h);
+
+/* Fused bias + tanh-GeLU (reading #3): out = gelu(y + b), y [R, N]. */
+mp_status mp_op_bias_gelu_fwd(mp_dtype dt, const void* y, const void* b, void* out, long long R, int N,
+                              void* stream);
+/* Its backward: du = dh * gelu'(y + b); db (fp32 [N]) += column sums of du. */
+mp_status mp_op_bias_gelu_bwd(mp_dtype dt, const void* dh, const void* y, const void* b, void* du, float* db, int R,
+                              int N, void* stream);
+
+/* Implicit-causal scale-mask-softmax in place over z matrices
+ * [s, s]: P[i, j] = exp(scale S[i,j]) / sum_{k<=i} exp(scale S[i,k]) for
+ * j <= i; reads only j <= i; writes j < kend(i) = min(s, 128 (floor(i/128)+1)),
+ * zeros for j > i.  s <= 4096 (bf16). */
+mp_status mp_op_softmax_causal_fwd(mp_dtype dt, void* S, long long z, int s, float scale, void* stream);
+/* Backward in place on dP: dS = P (dP - rowsum(dP P)) scale, same masking. */
+mp_status mp_op_softmax_causal_bwd(mp_dtype dt, void* dP, const void* P, long long z, int s, float scale,
+                                   void* stream);
+
+/* out[n] += sum_r X[r, n] (bias gradients, fp32 out). */
+mp_status mp_op_colsum_accum(mp_dtype dt, const void* X, float* out, int R, int N, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,0 +1,757 @@
+// Memory-bound kernels of the hot path; see kernels.cuh for the contracts.
+// Design: every kernel streams 16-byte vectors (8 bf16 or 4 fp32) with the
+// thread index on the contiguous dimension, keeps one row in registers where
+// the op is a row reduction (LayerNorm: one CTA per row; causal softmax: one
+// warp per row), reduces with warp shuffles, and computes in fp32.
+#include "kernels.cuh"
+#include "common.h"
+
+#include <algorithm>
+#include <cfloat>
+
+namespace mp {
+
+// ------------------------------------------------------------ vector I/O
+template <class T> struct VW;
+template <> struct VW<float> { static constexpr int N = 4; };
+template <> struct VW<__nv_bfloat16> { static constexpr int N = 8; };
+
+__device__ __forceinline__ void ld_vec(const float* p, float* o) {
+  float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+}
+__device__ __forceinline__ void st_vec(float* p, const float* o) {
+  *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+}
+__device__ __forceinline__ void ld_vec(const __nv_bfloat16* p, float* o) {
+  uint4 v = *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x; o[2 * i + 1] = f.y;
+  }
+}
+__device__ __forceinline__ void st_vec(__nv_bfloat16* p, const float* o) {
+  uint4 v;
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h[i] = __floats2bfloat162_rn(o[2 * i], o[2 * i + 1]);
+  *reinterpret_cast<uint4*>(p) = v;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+// Sum of two values over the block (<= 32 warps); result broadcast to all threads.
+__device__ __forceinline__ float2 block_sum2(float a, float b, float2* red) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32, nw = (blockDim.x + 31) / 32;
+  __syncthreads();
+  if (l == 0) red[w] = make_float2(a, b);
+  __syncthreads();
+  float2 r = make_float2(0.f, 0.f);
+  for (int i = 0; i < nw; ++i) { r.x += red[i].x; r.y += red[i].y; }
+  return r;
+}
+__device__ __forceinline__ float block_max(float a, float* red) {
+  a = warp_max(a);
+  const int w = threadIdx.x / 32, l = threadIdx.x % 32, nw = (blockDim.x + 31) / 32;
+  __syncthreads();
+  if (l == 0) red[w] = a;
+  __syncthreads();
+  float r = -FLT_MAX;
+  for (int i = 0; i < nw; ++i) r = fmaxf(r, red[i]);
+  return r;
+}
+
+static int row_threads(int nvec) {
+  int t = ((nvec + 3) / 4 + 31) / 32 * 32;   // <= 4 vectors per thread
+  return std::max(32, std::min(256, t));
+}
+constexpr int LN_MAXV = 4;
+
+#define LAUNCH_CHECK()                                                                         \
+  do {                                                                                         \
+    cudaError_t _e = cudaGetLastError();                                                       \
+    if (_e != cudaSuccess) return set_err(MP_ECUDA, "%s: %s", __func__, cudaGetErrorString(_e)); \
+    return MP_OK;                                                                              \
+  } while (0)
+
+// ------------------------------------------------------------ LayerNorm fwd
+// mode 0: x = in; mode 1: x = r + yv + bias (bias-dropout-add with p = 0), x1 <- x.
+template <class T, int MODE>
+__global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, const T* __restrict__ bias,
+                                                     const T* __restrict__ res, T* __restrict__ x1,
+                                                     const T* __restrict__ g, const T* __restrict__ b,
+                                                     T* __restrict__ out, float* __restrict__ mean,
+                                                     float* __restrict__ rstd, int h, float eps) {
+  constexpr int V = VW<T>::N;
+  __shared__ float2 red[32];
+  const long long row = blockIdx.x;
+  const int nvec = h / V;
+  float v[LN_MAXV][V];
+  float s1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      ld_vec(in + row * h + vi * V, v[k]);
+      if (MODE == 1) {
+        float bb[V], rr[V];
+        ld_vec(bias + vi * V, bb);
+        ld_vec(res + row * h + vi * V, rr);
+#pragma unroll
+        for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
+        st_vec(x1 + row * h + vi * V, v[k]);
+        // LayerNorm consumes the stored (rounded) residual stream value
+        ld_vec(x1 + row * h + vi * V, v[k]);
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) s1 += v[k][e];
+    }
+  }
+  const float mu = block_sum2(s1, 0.f, red).x / h;
+  float s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec)
+#pragma unroll
+      for (int e = 0; e < V; ++e) { float d = v[k][e] - mu; s2 += d * d; }
+  }
+  const float var = block_sum2(s2, 0.f, red).x / h;
+  const float rs = rsqrtf(var + eps);
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float gg[V], bb[V], o[V];
+      ld_vec(g + vi * V, gg);
+      ld_vec(b + vi * V, bb);
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = (v[k][e] - mu) * rs * gg[e] + bb[e];
+      st_vec(out + row * h + vi * V, o);
+    }
+  }
+  if (threadIdx.x == 0) { mean[row] = mu; rstd[row] = rs; }
+}
+
+template <class T>
+static mp_status check_row_dims(int R, int h) {
+  constexpr int V = VW<T>::N;
+  if (R <= 0 || h <= 0 || h % V) return set_err(MP_EINVAL, "row kernel: h=%d must be a multiple of %d", h, V);
+  if (h / V > LN_MAXV * 256) return set_err(MP_EINVAL, "row kernel: h=%d too large", h);
+  return MP_OK;
+}
+
+template <class T>
+mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int R, int h, float eps,
+                        cudaStream_t st) {
+  MP_TRY(check_row_dims<T>(R, h));
+  ln_fwd_kernel<T, 0><<<R, row_threads(h / VW<T>::N), 0, st>>>(x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, h,
+                                                                eps);
+  LAUNCH_CHECK();
+}
+
+template <class T>
+mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
+                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st) {
+  MP_TRY(check_row_dims<T>(R, h));
+  ln_fwd_kernel<T, 1><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps);
+  LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------ bias + residual add
+template <class T>
+__global__ void bias_add_residual_kernel(const T* __restrict__ yv, const T* __restrict__ bias,
+                                         const T* __restrict__ r, T* __restrict__ out, long long nvec, int hv) {
+  constexpr int V = VW<T>::N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    float a[V], bb[V], rr[V];
+    ld_vec(yv + i * V, a);
+    ld_vec(bias + (i % hv) * V, bb);
+    ld_vec(r + i * V, rr);
+#pragma unroll
+    for (int e = 0; e < V; ++e) a[e] = rr[e] + (a[e] + bb[e]);
+    st_vec(out + i * V, a);
+  }
+}
+
+static int ew_grid(long long nvec) {
+  long long g = (nvec + 255) / 256;
+  return (int)std::max(1LL, std::min<long long>(g, (long long)num_sms() * 8));
+}
+
+template <class T>
+mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (h % V) return set_err(MP_EINVAL, "bias_add_residual: h %% %d", V);
+  long long nvec = R * h / V;
+  bias_add_residual_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V);
+  LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------ LayerNorm bwd
+constexpr int LNB_ROWS = 16;
+
+template <class T>
+__global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                     const T* __restrict__ g, const float* __restrict__ mean,
+                                                     const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                     T* __restrict__ dx, float* __restrict__ part, int R, int h) {
+  constexpr int V = VW<T>::N;
+  __shared__ float2 red[32];
+  const int nvec = h / V;
+  float adg[LN_MAXV][V], adb[LN_MAXV][V], gg[LN_MAXV][V];
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+#pragma unroll
+    for (int e = 0; e < V; ++e) { adg[k][e] = 0.f; adb[k][e] = 0.f; gg[k][e] = 0.f; }
+    if (vi < nvec) ld_vec(g + vi * V, gg[k]);
+  }
+  const int r0 = blockIdx.x * LNB_ROWS;
+  for (int rr = 0; rr < LNB_ROWS; ++rr) {
+    const long long row = r0 + rr;
+    if (row >= R) break;
+    const float mu = mean[row], rs = rstd[row];
+    float xh[LN_MAXV][V], dxh[LN_MAXV][V];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < LN_MAXV; ++k) {
+      const int vi = threadIdx.x + k * blockDim.x;
+      if (vi < nvec) {
+        float d[V], xv[V];
+        ld_vec(dy + row * h + vi * V, d);
+        ld_vec(x + row * h + vi * V, xv);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          xh[k][e] = (xv[e] - mu) * rs;
+          dxh[k][e] = d[e] * gg[k][e];
+          s1 += dxh[k][e];
+          s2 += dxh[k][e] * xh[k][e];
+          adg[k][e] += d[e] * xh[k][e];
+          adb[k][e] += d[e];
+        }
+      }
+    }
+    const float2 s = block_sum2(s1, s2, red);
+    const float m1 = s.x / h, m2 = s.y / h;
+#pragma unroll
+    for (int k = 0; k < LN_MAXV; ++k) {
+      const int vi = threadIdx.x + k * blockDim.x;
+      if (vi < nvec) {
+        float o[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
+        if (dres) {
+          float q[V];
+          ld_vec(dres + row * h + vi * V, q);
+#pragma unroll
+          for (int e = 0; e < V; ++e) o[e] += q[e];
+        }
+        st_vec(dx + row * h + vi * V, o);
+      }
+    }
+  }
+  // per-CTA partial column sums: part[blockIdx.x][0][h] = dgamma, [1][h] = dbeta
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float* pg = part + (long long)blockIdx.x * 2 * h + vi * V;
+      st_vec(pg, adg[k]);
+      st_vec(pg + h, adb[k]);
+    }
+  }
+}
+
+// out[n] += sum_r X[r, n] over a [R, N] matrix: 2-D grid (column vectors x row chunks), fp32 atomics.
+constexpr int CS_ROWS = 64;
+template <class T>
+__global__ void colsum_kernel(const T* __restrict__ X, float* __restrict__ out, int R, int N) {
+  constexpr int V = VW<T>::N;
+  const int vi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (vi * V >= N) return;
+  float acc[V] = {};
+  const int r0 = blockIdx.y * CS_ROWS, r1 = min(R, r0 + CS_ROWS);
+  for (int r = r0; r < r1; ++r) {
+    float v[V];
+    ld_vec(X + (long long)r * N + vi * V, v);
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] += v[e];
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e) atomicAdd(out + vi * V + e, acc[e]);
+}
+
+template <class T>
+mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (N % V) return set_err(MP_EINVAL, "colsum: N %% %d", V);
+  const int nv = N / V;
+  const int bx = std::min(256, (nv + 31) / 32 * 32);
+  dim3 grid((nv + bx - 1) / bx, (R + CS_ROWS - 1) / CS_ROWS);
+  colsum_kernel<T><<<grid, bx, 0, st>>>(X, out, R, N);
+  LAUNCH_CHECK();
+}
+
+
+__global__ void colsum_strided_kernel(const float* __restrict__ X, float* __restrict__ out, int R, int N,
+                                      long long ld) {
+  const int vi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (vi * 4 >= N) return;
+  float acc[4] = {};
+  const int r0 = blockIdx.y * CS_ROWS, r1 = min(R, r0 + CS_ROWS);
+  for (int r = r0; r < r1; ++r) {
+    float v[4];
+    ld_vec(X + (long long)r * ld + vi * 4, v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[e] += v[e];
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) atomicAdd(out + vi * 4 + e, acc[e]);
+}
+
+template <class T>
+mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
+                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st) {
+  MP_TRY(check_row_dims<T>(R, h));
+  const int nb = (R + LNB_ROWS - 1) / LNB_ROWS;
+  ln_bwd_kernel<T><<<nb, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, scratch, R, h);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(MP_ECUDA, "ln_bwd: %s", cudaGetErrorString(e));
+  // reduce the [nb, 2, h] partials: view as nb rows of 2h columns into [dgamma | dbeta]
+  // (dgamma and dbeta are separate buffers, so reduce each half).
+  {
+    const int V = 4, nv = h / V;
+    const int bx = std::min(256, (nv + 31) / 32 * 32);
+    dim3 grid((nv + bx - 1) / bx, (nb + CS_ROWS - 1) / CS_ROWS);
+    // dgamma: rows of stride 2h starting at scratch; dbeta at scratch + h
+    colsum_strided_kernel<<<grid, bx, 0, st>>>(scratch, dgamma, nb, h, 2LL * h);
+    colsum_strided_kernel<<<grid, bx, 0, st>>>(scratch + h, dbeta, nb, h, 2LL * h);
+  }
+  LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------------- GeLU
+__device__ __forceinline__ float gelu_f(float u, float* dgelu) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float th = tanhf(c * (u + a * u * u * u));
+  if (dgelu) *dgelu = 0.5f * (1.f + th) + 0.5f * u * (1.f - th * th) * c * (1.f + 3.f * a * u * u);
+  return 0.5f * u * (1.f + th);
+}
+
+template <class T>
+__global__ void bias_gelu_fwd_kernel(const T* __restrict__ yv, const T* __restrict__ b, T* __restrict__ out,
+                                     long long nvec, int nv_row) {
+  constexpr int V = VW<T>::N;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
+    float a[V], bb[V];
+    ld_vec(yv + i * V, a);
+    ld_vec(b + (i % nv_row) * V, bb);
+#pragma unroll
+    for (int e = 0; e < V; ++e) a[e] = gelu_f(a[e] + bb[e], nullptr);
+    st_vec(out + i * V, a);
+  }
+}
+
+template <class T>
+mp_status bias_gelu_fwd(const T* yv, const T* b, T* out, long long R, int N, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (N % V) return set_err(MP_EINVAL, "bias_gelu: N %% %d", V);
+  long long nvec = R * N / V;
+  bias_gelu_fwd_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, b, out, nvec, N / V);
+  LAUNCH_CHECK();
+}
+
+template <class T>
+__global__ void bias_gelu_bwd_kernel(const T* dh, const T* __restrict__ yv, const T* __restrict__ b, T* du,
+                                     float* __restrict__ db, int R, int N) {  // du may alias dh
+  constexpr int V = VW<T>::N;
+  const int vi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (vi * V >= N) return;
+  float bb[V], acc[V] = {};
+  ld_vec(b + vi * V, bb);
+  const int r0 = blockIdx.y * CS_ROWS, r1 = min(R, r0 + CS_ROWS);
+  for (int r = r0; r < r1; ++r) {
+    float d[V], y[V];
+    const long long off = (long long)r * N + vi * V;
+    ld_vec(dh + off, d);
+    ld_vec(yv + off, y);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      float gd;
+      gelu_f(y[e] + bb[e], &gd);
+      d[e] *= gd;
+    }
+    st_vec(du + off, d);
+    // the bias gradient is the column sum of the stored (rounded) dU
+    ld_vec(du + off, d);
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] += d[e];
+  }
+#pragma unroll
+  for (int e = 0; e < V; ++e) atomicAdd(db + vi * V + e, acc[e]);
+}
+
+template <class T>
+mp_status bias_gelu_bwd(const T* dh, const T* yv, const T* b, T* du, float* db, int R, int N, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (N % V) return set_err(MP_EINVAL, "bias_gelu_bwd: N %% %d", V);
+  const int nv = N / V;
+  const int bx = std::min(256, (nv + 31) / 32 * 32);
+  dim3 grid((nv + bx - 1) / bx, (R + CS_ROWS - 1) / CS_ROWS);
+  bias_gelu_bwd_kernel<T><<<grid, bx, 0, st>>>(dh, yv, b, du, db, R, N);
+  LAUNCH_CHECK();
+}
+
+// ----------------------------------------------------- causal softmax
+// One warp per row i of a [z, s, s] score tensor; the row is held in
+// registers (MAXK vectors per lane).  Reads columns j <= i only, writes
+// columns j < kend(i) (zeros for j > i).  exp2 with the scale folded into log2e.
+template <class T, int MAXK>
+__global__ void __launch_bounds__(256) softmax_fwd_kernel(T* __restrict__ S, long long rows, int s, float scale_log2) {
+  constexpr int V = VW<T>::N;
+  const long long rg = blockIdx.x * 8LL + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (rg >= rows) return;
+  const int i = (int)(rg % s);
+  T* p = S + rg * s;
+  const int nv_read = i / V + 1;
+  const int nv_write = causal_kend(i, s) / V;
+  float v[MAXK][V];
+  float mx = -FLT_MAX;
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv_read) {
+      ld_vec(p + vi * V, v[k]);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const int col = vi * V + e;
+        v[k][e] = col <= i ? v[k][e] * scale_log2 : -FLT_MAX;
+        mx = fmaxf(mx, v[k][e]);
+      }
+    }
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv_read)
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        const int col = vi * V + e;
+        v[k][e] = col <= i ? exp2f(v[k][e] - mx) : 0.f;
+        sum += v[k][e];
+      }
+  }
+  const float inv = 1.f / warp_sum(sum);
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv_write) {
+      float o[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = vi < nv_read ? v[k][e] * inv : 0.f;
+      st_vec(p + vi * V, o);
+    }
+  }
+  // columns beyond the register window (only when s > 32*MAXK*V, never with the dispatch below)
+}
+
+template <class T, int MAXK>
+__global__ void __launch_bounds__(256) softmax_bwd_kernel(T* __restrict__ dP, const T* __restrict__ P, long long rows,
+                                                          int s, float scale) {
+  constexpr int V = VW<T>::N;
+  const long long rg = blockIdx.x * 8LL + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (rg >= rows) return;
+  const int i = (int)(rg % s);
+  T* dp = dP + rg * s;
+  const T* pp = P + rg * s;
+  const int nv_read = i / V + 1;
+  const int nv_write = causal_kend(i, s) / V;
+  float d[MAXK][V], pv[MAXK][V];
+  float dot = 0.f;
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv_read) {
+      ld_vec(dp + vi * V, d[k]);
+      ld_vec(pp + vi * V, pv[k]);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        if (vi * V + e > i) { d[k][e] = 0.f; pv[k][e] = 0.f; }
+        dot += d[k][e] * pv[k][e];
+      }
+    }
+  }
+  dot = warp_sum(dot);
+#pragma unroll
+  for (int k = 0; k < MAXK; ++k) {
+    const int vi = lane + 32 * k;
+    if (vi < nv_write) {
+      float o[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = vi < nv_read ? pv[k][e] * (d[k][e] - dot) * scale : 0.f;
+      st_vec(dp + vi * V, o);
+    }
+  }
+}
+
+template <class T>
+static int softmax_maxk(int s) {
+  constexpr int V = VW<T>::N;
+  int need = (s + 32 * V - 1) / (32 * V);
+  for (int k : {1, 2, 4, 8, 16})
+    if (k >= need) return k;
+  return -1;
+}
+
+template <class T>
+mp_status softmax_causal_fwd(T* S, long long z, int s, float scale, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (s % V) return set_err(MP_EINVAL, "softmax: s %% %d", V);
+  const int mk = softmax_maxk<T>(s);
+  if (mk < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
+  const long long rows = z * s;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  const float sl2 = scale * 1.4426950408889634f;
+  switch (mk) {
+    case 1: softmax_fwd_kernel<T, 1><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
+    case 2: softmax_fwd_kernel<T, 2><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
+    case 4: softmax_fwd_kernel<T, 4><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
+    case 8: softmax_fwd_kernel<T, 8><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
+    default: softmax_fwd_kernel<T, 16><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
+  }
+  LAUNCH_CHECK();
+}
+
+template <class T>
+mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (s % V) return set_err(MP_EINVAL, "softmax: s %% %d", V);
+  const int mk = softmax_maxk<T>(s);
+  if (mk < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
+  const long long rows = z * s;
+  const unsigned grid = (unsigned)((rows + 7) / 8);
+  switch (mk) {
+    case 1: softmax_bwd_kernel<T, 1><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
+    case 2: softmax_bwd_kernel<T, 2><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
+    case 4: softmax_bwd_kernel<T, 4><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
+    case 8: softmax_bwd_kernel<T, 8><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
+    default: softmax_bwd_kernel<T, 16><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
+  }
+  LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------- embedding
+template <class T>
+__global__ void embed_fwd_kernel(const int* __restrict__ tok, int tok_ld, const T* __restrict__ E, int v0, int Vr,
+                                 const T* __restrict__ pos, T* __restrict__ X, int b, int h) {
+  constexpr int V = VW<T>::N;
+  const int row = blockIdx.x;           // row = i*b + beta
+  const int i = row / b, beta = row % b;
+  const int id = tok[(long long)beta * tok_ld + i] - v0;
+  const bool own = id >= 0 && id < Vr;
+  for (int vi = threadIdx.x; vi < h / V; vi += blockDim.x) {
+    float o[V] = {};
+    if (own) ld_vec(E + (long long)id * h + vi * V, o);
+    if (pos) {
+      float q[V];
+      ld_vec(pos + (long long)i * h + vi * V, q);
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] += q[e];
+    }
+    st_vec(X + (long long)row * h + vi * V, o);
+  }
+}
+
+template <class T>
+mp_status embed_fwd(const int* tok, int tok_ld, const T* E, int v0, int Vr, const T* pos, T* X, int s, int b, int h,
+                    cudaStream_t st) {
+  if (h % VW<T>::N) return set_err(MP_EINVAL, "embed: h");
+  embed_fwd_kernel<T><<<s * b, std::min(256, std::max(32, h / VW<T>::N)), 0, st>>>(tok, tok_ld, E, v0, Vr, pos, X, b,
+                                                                                    h);
+  LAUNCH_CHECK();
+}
+
+template <class T>
+__global__ void embed_bwd_kernel(const int* __restrict__ tok, int tok_ld, const T* __restrict__ dX, int v0, int Vr,
+                                 float* __restrict__ dE, float* __restrict__ dpos, int b, int h) {
+  constexpr int V = VW<T>::N;
+  const int row = blockIdx.x;
+  const int i = row / b, beta = row % b;
+  const int id = tok[(long long)beta * tok_ld + i] - v0;
+  const bool own = id >= 0 && id < Vr;
+  for (int vi = threadIdx.x; vi < h / V; vi += blockDim.x) {
+    float d[V];
+    ld_vec(dX + (long long)row * h + vi * V, d);
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      if (own) atomicAdd(dE + (long long)id * h + vi * V + e, d[e]);
+      if (dpos) atomicAdd(dpos + (long long)i * h + vi * V + e, d[e]);
+    }
+  }
+}
+
+template <class T>
+mp_status embed_bwd(const int* tok, int tok_ld, const T* dX, int v0, int Vr, float* dE, float* dpos, int s, int b,
+                    int h, cudaStream_t st) {
+  if (h % VW<T>::N) return set_err(MP_EINVAL, "embed: h");
+  embed_bwd_kernel<T><<<s * b, std::min(256, std::max(32, h / VW<T>::N)), 0, st>>>(tok, tok_ld, dX, v0, Vr, dE, dpos,
+                                                                                    b, h);
+  LAUNCH_CHECK();
+}
+
+// ---------------------------------------------------------- cross-entropy
+__global__ void ce_rowmax_kernel(const float* __restrict__ L, float* __restrict__ rowmax, int Vr) {
+  __shared__ float red[32];
+  const float* p = L + (long long)blockIdx.x * Vr;
+  float m = -FLT_MAX;
+  for (int j = threadIdx.x * 4; j < Vr; j += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(p + j);
+    m = fmaxf(m, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
+  }
+  m = block_max(m, red);
+  if (threadIdx.x == 0) rowmax[blockIdx.x] = m;
+}
+
+mp_status ce_rowmax(const float* logits, float* rowmax, int R, int Vr, cudaStream_t st) {
+  if (Vr % 4) return set_err(MP_EINVAL, "ce: Vr %% 4");
+  ce_rowmax_kernel<<<R, 256, 0, st>>>(logits, rowmax, Vr);
+  LAUNCH_CHECK();
+}
+
+__device__ __forceinline__ int ce_label(const int* lab, int lab_ld, int row, int b) {
+  return lab[(long long)(row % b) * lab_ld + row / b];
+}
+
+__global__ void ce_sum_kernel(const float* __restrict__ L, const float* __restrict__ rowmax,
+                              const int* __restrict__ lab, int lab_ld, int b, int v0, float* __restrict__ out, int R,
+                              int Vr) {
+  __shared__ float2 red[32];
+  const int row = blockIdx.x;
+  const float* p = L + (long long)row * Vr;
+  const float mx = rowmax[row];
+  float s = 0.f;
+  for (int j = threadIdx.x * 4; j < Vr; j += blockDim.x * 4) {
+    float4 v = *reinterpret_cast<const float4*>(p + j);
+    s += __expf(v.x - mx) + __expf(v.y - mx) + __expf(v.z - mx) + __expf(v.w - mx);
+  }
+  s = block_sum2(s, 0.f, red).x;
+  if (threadIdx.x == 0) {
+    const int id = ce_label(lab, lab_ld, row, b) - v0;
+    out[row] = s;
+    out[R + row] = (id >= 0 && id < Vr) ? p[id] : 0.f;
+  }
+}
+
+mp_status ce_sumexp_target(const float* logits, const float* rowmax, const int* lab, int lab_ld, int s, int b, int v0,
+                           float* sum_tgt, int R, int Vr, cudaStream_t st) {
+  ce_sum_kernel<<<R, 256, 0, st>>>(logits, rowmax, lab, lab_ld, b, v0, sum_tgt, R, Vr);
+  LAUNCH_CHECK();
+}
+
+template <class T>
+__global__ void ce_grad_kernel(const float* __restrict__ L, const float* __restrict__ rowmax,
+                               const float* __restrict__ st, const int* __restrict__ lab, int lab_ld, int b, int v0,
+                               float scale, T* __restrict__ dL, float* __restrict__ loss_acc, int R, int Vr) {
+  constexpr int V = VW<T>::N;
+  const int row = blockIdx.x;
+  const float* p = L + (long long)row * Vr;
+  const float mx = rowmax[row], sum = st[row];
+  const float inv = 1.f / sum;
+  const int id = ce_label(lab, lab_ld, row, b) - v0;
+  if (threadIdx.x == 0) atomicAdd(loss_acc, scale * (logf(sum) + mx - st[R + row]));
+  for (int j = threadIdx.x * V; j < Vr; j += blockDim.x * V) {
+    float o[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) o[e] = (__expf(p[j + e] - mx) * inv - (j + e == id ? 1.f : 0.f)) * scale;
+    st_vec(dL + (long long)row * Vr + j, o);
+  }
+}
+
+template <class T>
+mp_status ce_loss_grad(const float* logits, const float* rowmax, const float* sum_tgt, const int* lab, int lab_ld,
+                       int s, int b, int v0, float scale, T* dlogits, float* loss_acc, int R, int Vr, cudaStream_t st) {
+  if (Vr % VW<T>::N) return set_err(MP_EINVAL, "ce: Vr");
+  ce_grad_kernel<T><<<R, 256, 0, st>>>(logits, rowmax, sum_tgt, lab, lab_ld, b, v0, scale, dlogits, loss_acc, R, Vr);
+  LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------------------ Adam
+template <class T>
+__global__ void adam_kernel(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m1,
+                            float* __restrict__ m2, T* __restrict__ ws, long long n, float lr, float b1, float b2,
+                            float eps, float bc1, float bc2) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const float gi = g[i];
+    const float a = b1 * m1[i] + (1.f - b1) * gi;
+    const float c = b2 * m2[i] + (1.f - b2) * gi * gi;
+    m1[i] = a;
+    m2[i] = c;
+    const float wn = w[i] - lr * (a / bc1) / (sqrtf(c / bc2) + eps);
+    w[i] = wn;
+    if constexpr (sizeof(T) == 2) ws[i] = __float2bfloat16_rn(wn); else ws[i] = wn;
+  }
+}
+
+template <class T>
+mp_status adam_step(float* w, const float* g, float* m1, float* m2, T* w_store, long long n, float lr, float b1,
+                    float b2, float eps, float bc1, float bc2, cudaStream_t st) {
+  adam_kernel<T><<<ew_grid(n), 256, 0, st>>>(w, g, m1, m2, w_store, n, lr, b1, b2, eps, bc1, bc2);
+  LAUNCH_CHECK();
+}
+
+template <class T>
+__global__ void cast_kernel(const float* __restrict__ s, T* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if constexpr (sizeof(T) == 2) d[i] = __float2bfloat16_rn(s[i]); else d[i] = s[i];
+  }
+}
+
+template <class T>
+mp_status cast_from_f32(const float* src, T* dst, long long n, cudaStream_t st) {
+  cast_kernel<T><<<ew_grid(n), 256, 0, st>>>(src, dst, n);
+  LAUNCH_CHECK();
+}
+
+// ------------------------------------------------------ instantiations
+#define INST(T)                                                                                                     \
+  template mp_status layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, float,             \
+                                      cudaStream_t);                                                                \
+  template mp_status bda_layernorm_fwd<T>(const T*, const T*, const T*, T*, const T*, const T*, T*, float*, float*,  \
+                                          int, int, float, cudaStream_t);                                           \
+  template mp_status bias_add_residual<T>(const T*, const T*, const T*, T*, long long, int, cudaStream_t);           \
+  template mp_status layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*,        \
+                                      float*, float*, float*, int, int, cudaStream_t);                              \
+  template mp_status bias_gelu_fwd<T>(const T*, const T*, T*, long long, int, cudaStream_t);                         \
+  template mp_status bias_gelu_bwd<T>(const T*, const T*, const T*, T*, float*, int, int, cudaStream_t);             \
+  template mp_status colsum_accum<T>(const T*, float*, int, int, cudaStream_t);                                     \
+  template mp_status softmax_causal_fwd<T>(T*, long long, int, float, cudaStream_t);                                \
+  template mp_status softmax_causal_bwd<T>(T*, const T*, long long, int, float, cudaStream_t);                      \
+  template mp_status embed_fwd<T>(const int*, int, const T*, int, int, const T*, T*, int, int, int, cudaStream_t);  \
+  template mp_status embed_bwd<T>(const int*, int, const T*, int, int, float*, float*, int, int, int, cudaStream_t); \
+  template mp_status ce_loss_grad<T>(const float*, const float*, const float*, const int*, int, int, int, int,      \
+                                     float, T*, float*, int, int, cudaStream_t);                                    \
+  template mp_status adam_step<T>(float*, const float*, float*, float*, T*, long long, float, float, float, float,  \
+                                  float, float, cudaStream_t);                                                      \
+  template mp_status cast_from_f32<T>(const float*, T*, long long, cudaStream_t);
+
+INST(float)
+INST(__nv_bfloat16)
+
+}  // namespace mp

@@ -1,0 +1,366 @@
+// Tensor-parallel GPT transformer layer (Megatron partitioning),
+// model ends (vocab-parallel embedding, final LayerNorm + tied logit layer +
+// cross-entropy), forward and backward, on one rank of a TP group.
+//
+// Forward (per rank, T = s*b rows, [s, b, h] layout):
+//   A   = LN1(X)                               replicated          (a4)
+//   QKV = A Wqkv_r^T + bqkv_r                  column-parallel     (a6)
+//   S   = Q K^T per head (causal tile skip)    strided batched     (a7)
+//   P   = softmax(S / sqrt(hd)), in place      fused kernel        (a8)
+//   ctx = P V                                  strided batched     (a9)
+//   Z   = ctx Wo_r^T                           row-parallel        (a10)
+//   g: all-reduce(Z)                           NCCL, TP comm       (a11)
+//   X1 = X + Z + bo; A2 = LN2(X1)              fused kernel        (a12, a13)
+//   Y1 = A2 W1_r^T; H = gelu(Y1 + b1)          column-parallel + fused (a14, a15)
+//   Z   = H W2_r^T; g: all-reduce; Y = X1 + Z + b2                  (a16)
+// Backward mirrors it (a17); the two f all-reduces of the LayerNorm-input
+// gradients run on a side stream concurrently with the matching dW GEMM.
+#include <cmath>
+
+#include "common.h"
+#include "kernels.cuh"
+#include "layer.h"
+#include "../../include/mp_ops.h"
+
+namespace mp {
+
+mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st);
+
+static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+mp_status nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) return set_err(MP_ENCCL, "%s: %s", what, ncclGetErrorString(r));
+  return MP_OK;
+}
+
+// Y[T, N] = X[T, K] W[N, K]^T (+ bias)
+static mp_status lin_fwd(mp_ctx* c, const void* X, const void* W, const void* bias, void* Y, int T, int N, int K) {
+  mp_gemm_desc g{};
+  g.M = T; g.N = N; g.K = K; g.batch = 1;
+  g.A = X; g.lda = K; g.B = W; g.ldb = K; g.C = Y; g.ldc = N;
+  g.bias = bias; g.alpha = 1.f;
+  g.c_fp32 = c->cfg.dtype == MP_FP32;
+  return gemm(c->cfg.dtype, g, c->cs);
+}
+// dX[T, K] = dY[T, N] W[N, K]
+static mp_status lin_dgrad(mp_ctx* c, const void* dY, const void* W, void* dX, int T, int N, int K) {
+  mp_gemm_desc g{};
+  g.M = T; g.N = K; g.K = N; g.batch = 1;
+  g.A = dY; g.lda = N; g.a_major = 0;
+  g.B = W; g.ldb = K; g.b_major = 1;
+  g.C = dX; g.ldc = K; g.alpha = 1.f;
+  g.c_fp32 = c->cfg.dtype == MP_FP32;
+  return gemm(c->cfg.dtype, g, c->cs);
+}
+// dW[N, K] += dY[T, N]^T X[T, K]  (fp32 accumulators)
+static mp_status lin_wgrad(mp_ctx* c, const void* dY, const void* X, float* dW, int T, int N, int K) {
+  mp_gemm_desc g{};
+  g.M = N; g.N = K; g.K = T; g.batch = 1;
+  g.A = dY; g.lda = N; g.a_major = 1;
+  g.B = X; g.ldb = K; g.b_major = 1;
+  g.C = dW; g.ldc = K; g.c_fp32 = 1; g.accumulate = 1; g.alpha = 1.f;
+  return gemm(c->cfg.dtype, g, c->cs);
+}
+
+template <class T> static T* ptr(mp_ctx* c, int pidx) {
+  return reinterpret_cast<T*>(c->wstore) + c->params[pidx].off;
+}
+static float* gptr(mp_ctx* c, int pidx) { return c->grads + c->params[pidx].off; }
+
+enum { P_LN1G, P_LN1B, P_WQKV, P_BQKV, P_WO, P_BO, P_LN2G, P_LN2B, P_W1, P_B1, P_W2, P_B2 };
+
+struct Dims {
+  int T, h, ht, h3t, h4t, heads, hd, s, b;
+  long long z, sq;
+};
+static Dims dims(mp_ctx* c, int b) {
+  Dims d;
+  d.s = c->cfg.s; d.b = b; d.T = c->cfg.s * b; d.h = c->cfg.h;
+  d.ht = d.h / c->t; d.h3t = 3 * d.ht; d.h4t = 4 * d.ht;
+  d.heads = c->cfg.a / c->t; d.hd = d.h / c->cfg.a;
+  d.z = (long long)b * d.heads; d.sq = (long long)d.s * d.s;
+  return d;
+}
+
+mp_status alloc_async(mp_ctx* c, void** p, size_t bytes, cudaStream_t st) {
+  cudaError_t e = cudaMallocFromPoolAsync(p, bytes ? bytes : 256, c->pool, st);
+  if (e != cudaSuccess) return set_err(MP_ENOMEM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  return MP_OK;
+}
+
+mp_status ensure_workspace(mp_ctx* c, int b) {
+  if (c->ws_b >= b) return MP_OK;
+  MP_CUDA(cudaStreamSynchronize(c->cs));
+  void** bufs[] = {&c->ws_z, &c->ws_dsq, &c->ws_d4h, &c->ws_dh1, &c->ws_dh2, &c->ws_dqkv, &c->ws_dctx};
+  for (void** q : bufs)
+    if (*q) { cudaFree(*q); *q = nullptr; }
+  if (c->ws_ln) { cudaFree(c->ws_ln); c->ws_ln = nullptr; }
+  Dims d = dims(c, b);
+  const size_t es = c->esz;
+  size_t sizes[] = {(size_t)d.T * d.h * es, (size_t)(d.z * d.sq) * es, (size_t)d.T * d.h4t * es,
+                    (size_t)d.T * d.h * es, (size_t)d.T * d.h * es, (size_t)d.T * d.h3t * es,
+                    (size_t)d.T * d.ht * es};
+  for (int i = 0; i < 7; ++i) MP_CUDA(cudaMalloc(bufs[i], al256(sizes[i])));
+  MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * mp_op_layernorm_bwd_scratch_floats(d.T, d.h))));
+  c->ws_b = b;
+  return MP_OK;
+}
+
+static mp_status allreduce(mp_ctx* c, void* buf, size_t n, cudaStream_t st) {
+  if (c->t == 1) return MP_OK;
+  return nccl_check(ncclAllReduce(buf, buf, n, c->nccl_dt, ncclSum, c->tp_comm, st), "tp all-reduce");
+}
+
+// ------------------------------------------------------------ attention
+template <class T>
+static mp_status attention_fwd(mp_ctx* c, const Dims& d, const void* QKV, void* P, void* ctx) {
+  const mp_dtype dt = c->cfg.dtype;
+  const long long ldq = (long long)d.b * d.h3t;
+  mp_gemm_desc g{};
+  // S = Q K^T  [z, s, s] (tiles above the diagonal skipped)
+  g.M = d.s; g.N = d.s; g.K = d.hd; g.batch = (int)d.z;
+  g.A = QKV; g.lda = ldq; g.strideA = 3LL * d.hd;
+  g.B = reinterpret_cast<const T*>(QKV) + d.hd; g.ldb = ldq; g.strideB = 3LL * d.hd;
+  g.C = P; g.ldc = d.s; g.strideC = d.sq; g.alpha = 1.f; g.causal = 1;
+  g.c_fp32 = dt == MP_FP32;
+  MP_TRY(gemm(dt, g, c->cs));
+  MP_TRY(softmax_causal_fwd<T>(reinterpret_cast<T*>(P), d.z, d.s, 1.f / std::sqrt((float)d.hd), c->cs));
+  // ctx = P V  [s, b, heads, hd]
+  g = mp_gemm_desc{};
+  g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
+  g.A = P; g.lda = d.s; g.strideA = d.sq;
+  g.B = reinterpret_cast<const T*>(QKV) + 2 * d.hd; g.ldb = ldq; g.strideB = 3LL * d.hd; g.b_major = 1;
+  g.C = ctx; g.ldc = (long long)d.b * d.ht; g.strideC = d.hd; g.alpha = 1.f; g.causal = 2;
+  g.c_fp32 = dt == MP_FP32;
+  return gemm(dt, g, c->cs);
+}
+
+template <class T>
+static mp_status attention_bwd(mp_ctx* c, const Dims& d, const void* QKV, const void* P, const void* dctx,
+                               void* dP, void* dQKV) {
+  const mp_dtype dt = c->cfg.dtype;
+  const bool f32 = dt == MP_FP32;
+  const long long ldq = (long long)d.b * d.h3t, ldc = (long long)d.b * d.ht;
+  const T* Q = reinterpret_cast<const T*>(QKV);
+  T* dQ = reinterpret_cast<T*>(dQKV);
+  mp_gemm_desc g{};
+  // dP = dO V^T (causal tiles)
+  g.M = d.s; g.N = d.s; g.K = d.hd; g.batch = (int)d.z;
+  g.A = dctx; g.lda = ldc; g.strideA = d.hd;
+  g.B = Q + 2 * d.hd; g.ldb = ldq; g.strideB = 3LL * d.hd;
+  g.C = dP; g.ldc = d.s; g.strideC = d.sq; g.alpha = 1.f; g.causal = 1; g.c_fp32 = f32;
+  MP_TRY(gemm(dt, g, c->cs));
+  // dV = P^T dO
+  g = mp_gemm_desc{};
+  g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
+  g.A = P; g.lda = d.s; g.strideA = d.sq; g.a_major = 1;
+  g.B = dctx; g.ldb = ldc; g.strideB = d.hd; g.b_major = 1;
+  g.C = dQ + 2 * d.hd; g.ldc = ldq; g.strideC = 3LL * d.hd; g.alpha = 1.f; g.causal = 3; g.c_fp32 = f32;
+  MP_TRY(gemm(dt, g, c->cs));
+  // dS = P (dP - rowsum(dP P)) / sqrt(hd), in place
+  MP_TRY(softmax_causal_bwd<T>(reinterpret_cast<T*>(dP), reinterpret_cast<const T*>(P), d.z, d.s,
+                               1.f / std::sqrt((float)d.hd), c->cs));
+  // dQ = dS K
+  g = mp_gemm_desc{};
+  g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
+  g.A = dP; g.lda = d.s; g.strideA = d.sq;
+  g.B = Q + d.hd; g.ldb = ldq; g.strideB = 3LL * d.hd; g.b_major = 1;
+  g.C = dQ; g.ldc = ldq; g.strideC = 3LL * d.hd; g.alpha = 1.f; g.causal = 2; g.c_fp32 = f32;
+  MP_TRY(gemm(dt, g, c->cs));
+  // dK = dS^T Q
+  g = mp_gemm_desc{};
+  g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
+  g.A = dP; g.lda = d.s; g.strideA = d.sq; g.a_major = 1;
+  g.B = Q; g.ldb = ldq; g.strideB = 3LL * d.hd; g.b_major = 1;
+  g.C = dQ + d.hd; g.ldc = ldq; g.strideC = 3LL * d.hd; g.alpha = 1.f; g.causal = 3; g.c_fp32 = f32;
+  return gemm(dt, g, c->cs);
+}
+
+// ------------------------------------------------------------- layer
+template <class T>
+static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y, LayerStash& st) {
+  const Dims d = dims(c, b);
+  const auto& lp = c->layer_params.at(layer).idx;
+  MP_TRY(ensure_workspace(c, b));
+  const size_t es = c->esz;
+  // one block for every stashed activation of this layer
+  size_t off[13], tot = 0;
+  size_t sz[13] = {4ull * d.T, 4ull * d.T, 4ull * d.T, 4ull * d.T, es * d.T * d.h, es * d.T * d.h3t,
+                   es * (size_t)(d.z * d.sq), es * d.T * d.ht, es * d.T * d.h, es * d.T * d.h, es * d.T * d.h4t,
+                   es * d.T * d.h4t, 0};
+  for (int i = 0; i < 12; ++i) { off[i] = tot; tot += al256(sz[i]); }
+  MP_TRY(alloc_async(c, &st.block, tot, c->cs));
+  char* base = reinterpret_cast<char*>(st.block);
+  st.mu1 = (float*)(base + off[0]); st.rs1 = (float*)(base + off[1]);
+  st.mu2 = (float*)(base + off[2]); st.rs2 = (float*)(base + off[3]);
+  st.A = base + off[4]; st.QKV = base + off[5]; st.P = base + off[6]; st.ctx = base + off[7];
+  st.X1 = base + off[8]; st.A2 = base + off[9]; st.Y1 = base + off[10]; st.H = base + off[11];
+  st.b = b;
+  const float eps = c->cfg.ln_eps;
+  const T* X = reinterpret_cast<const T*>(x);
+  MP_TRY(layernorm_fwd<T>(X, ptr<T>(c, lp[P_LN1G]), ptr<T>(c, lp[P_LN1B]), (T*)st.A, st.mu1, st.rs1, d.T, d.h, eps,
+                          c->cs));
+  MP_TRY(lin_fwd(c, st.A, ptr<T>(c, lp[P_WQKV]), ptr<T>(c, lp[P_BQKV]), st.QKV, d.T, d.h3t, d.h));
+  MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx));
+  MP_TRY(lin_fwd(c, st.ctx, ptr<T>(c, lp[P_WO]), nullptr, c->ws_z, d.T, d.h, d.ht));
+  MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
+  MP_TRY(bda_layernorm_fwd<T>((const T*)c->ws_z, ptr<T>(c, lp[P_BO]), X, (T*)st.X1, ptr<T>(c, lp[P_LN2G]),
+                              ptr<T>(c, lp[P_LN2B]), (T*)st.A2, st.mu2, st.rs2, d.T, d.h, eps, c->cs));
+  MP_TRY(lin_fwd(c, st.A2, ptr<T>(c, lp[P_W1]), nullptr, st.Y1, d.T, d.h4t, d.h));
+  MP_TRY(bias_gelu_fwd<T>((const T*)st.Y1, ptr<T>(c, lp[P_B1]), (T*)st.H, d.T, d.h4t, c->cs));
+  MP_TRY(lin_fwd(c, st.H, ptr<T>(c, lp[P_W2]), nullptr, c->ws_z, d.T, d.h, d.h4t));
+  MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
+  MP_TRY(bias_add_residual<T>((const T*)c->ws_z, ptr<T>(c, lp[P_B2]), (const T*)st.X1, (T*)y, d.T, d.h, c->cs));
+  return MP_OK;
+}
+
+template <class T>
+static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const void* dy, void* dx) {
+  const Dims d = dims(c, st.b);
+  const auto& lp = c->layer_params.at(layer).idx;
+  MP_TRY(ensure_workspace(c, st.b));
+  const T* dY = reinterpret_cast<const T*>(dy);
+  T* dU = (T*)c->ws_d4h;
+  T* dA2 = (T*)c->ws_dh1;
+  T* dX1 = (T*)c->ws_dh2;
+  cudaEvent_t ev_a = c->events.at(0), ev_b = c->events.at(1);
+  // MLP: dZ2 = dY (dropout p = 0); db2; dH = dY W2; dW2 += H^T dY
+  MP_TRY(colsum_accum<T>(dY, gptr(c, lp[P_B2]), d.T, d.h, c->cs));
+  MP_TRY(lin_dgrad(c, dY, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
+  MP_TRY(lin_wgrad(c, dY, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
+  MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]), d.T, d.h4t, c->cs));
+  MP_TRY(lin_dgrad(c, dU, ptr<T>(c, lp[P_W1]), dA2, d.T, d.h4t, d.h));
+  // f: all-reduce dA2 on the side stream while dW1 accumulates
+  if (c->t > 1) {
+    MP_CUDA(cudaEventRecord(ev_a, c->cs));
+    MP_CUDA(cudaStreamWaitEvent(c->side, ev_a, 0));
+    MP_TRY(allreduce(c, dA2, (size_t)d.T * d.h, c->side));
+    MP_CUDA(cudaEventRecord(ev_b, c->side));
+  }
+  MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
+  if (c->t > 1) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
+  MP_TRY(layernorm_bwd<T>(dA2, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
+                          gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs));
+  // attention block: dZ1 = dX1; dbo; dctx = dX1 Wo; dWo += ctx^T dX1
+  MP_TRY(colsum_accum<T>(dX1, gptr(c, lp[P_BO]), d.T, d.h, c->cs));
+  MP_TRY(lin_dgrad(c, dX1, ptr<T>(c, lp[P_WO]), c->ws_dctx, d.T, d.h, d.ht));
+  MP_TRY(lin_wgrad(c, dX1, st.ctx, gptr(c, lp[P_WO]), d.T, d.h, d.ht));
+  MP_TRY(attention_bwd<T>(c, d, st.QKV, st.P, c->ws_dctx, c->ws_dsq, c->ws_dqkv));
+  MP_TRY(colsum_accum<T>((const T*)c->ws_dqkv, gptr(c, lp[P_BQKV]), d.T, d.h3t, c->cs));
+  T* dA = (T*)c->ws_dh1;
+  MP_TRY(lin_dgrad(c, c->ws_dqkv, ptr<T>(c, lp[P_WQKV]), dA, d.T, d.h3t, d.h));
+  if (c->t > 1) {
+    MP_CUDA(cudaEventRecord(ev_a, c->cs));
+    MP_CUDA(cudaStreamWaitEvent(c->side, ev_a, 0));
+    MP_TRY(allreduce(c, dA, (size_t)d.T * d.h, c->side));
+    MP_CUDA(cudaEventRecord(ev_b, c->side));
+  }
+  MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
+  if (c->t > 1) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
+  MP_TRY(layernorm_bwd<T>(dA, (const T*)st.x, ptr<T>(c, lp[P_LN1G]), st.mu1, st.rs1, dX1, (T*)dx,
+                          gptr(c, lp[P_LN1G]), gptr(c, lp[P_LN1B]), c->ws_ln, d.T, d.h, c->cs));
+  return MP_OK;
+}
+
+mp_status layer_fwd(mp_ctx* c, int layer, int b, const void* x, void* y, LayerStash& st) {
+  return c->cfg.dtype == MP_BF16 ? layer_fwd_t<__nv_bfloat16>(c, layer, b, x, y, st)
+                                 : layer_fwd_t<float>(c, layer, b, x, y, st);
+}
+mp_status layer_bwd(mp_ctx* c, int layer, const LayerStash& st, const void* dy, void* dx) {
+  return c->cfg.dtype == MP_BF16 ? layer_bwd_t<__nv_bfloat16>(c, layer, st, dy, dx)
+                                 : layer_bwd_t<float>(c, layer, st, dy, dx);
+}
+mp_status stash_release(mp_ctx* c, LayerStash& st, cudaStream_t s) {
+  if (st.block) MP_CUDA(cudaFreeAsync(st.block, s));
+  if (st.own_x && st.x) MP_CUDA(cudaFreeAsync(st.x, s));
+  st = LayerStash{};
+  return MP_OK;
+}
+
+// ------------------------------------------------------------ model ends
+// Embedding (stage 0): X0 = E_r[tok] (vocab-parallel, rows [tp V/t, (tp+1) V/t))
+// + pos (added by tp rank 0), then all-reduce over the TP group.
+template <class T>
+static mp_status embed_fwd_t(mp_ctx* c, const int* dtok, int tok_ld, int b, void* X) {
+  const int Vr = c->cfg.V / c->t;
+  const int ie = c->param_index.at("emb#-1"), ip = c->param_index.at("pos#-1");
+  MP_TRY(embed_fwd<T>(dtok, tok_ld, ptr<T>(c, ie), c->tp * Vr, Vr, c->tp == 0 ? ptr<T>(c, ip) : nullptr, (T*)X,
+                      c->cfg.s, b, c->cfg.h, c->cs));
+  return allreduce(c, X, (size_t)c->cfg.s * b * c->cfg.h, c->cs);
+}
+template <class T>
+static mp_status embed_bwd_t(mp_ctx* c, const int* dtok, int tok_ld, int b, const void* dX) {
+  const int Vr = c->cfg.V / c->t;
+  const int ie = c->param_index.at("emb#-1"), ip = c->param_index.at("pos#-1");
+  return embed_bwd<T>(dtok, tok_ld, (const T*)dX, c->tp * Vr, Vr, gptr(c, ie), gptr(c, ip), c->cfg.s, b, c->cfg.h,
+                      c->cs);
+}
+mp_status embed_forward(mp_ctx* c, const int* dtok, int tok_ld, int b, void* X) {
+  return c->cfg.dtype == MP_BF16 ? embed_fwd_t<__nv_bfloat16>(c, dtok, tok_ld, b, X)
+                                 : embed_fwd_t<float>(c, dtok, tok_ld, b, X);
+}
+mp_status embed_backward(mp_ctx* c, const int* dtok, int tok_ld, int b, const void* dX) {
+  return c->cfg.dtype == MP_BF16 ? embed_bwd_t<__nv_bfloat16>(c, dtok, tok_ld, b, dX)
+                                 : embed_bwd_t<float>(c, dtok, tok_ld, b, dX);
+}
+
+// Head (last stage): Z = LN_f(X); logits = Z E_r^T (fp32, [T, V/t]);
+// vocab-parallel cross-entropy (TP all-reduces of row max, sum-exp and
+// target logit); dlogits = (softmax - onehot) * scale; dZ = dlogits E_r
+// (f: all-reduce); dE_r += dlogits^T Z; dX = LN_f'(dZ).  loss += scale * sum.
+template <class T>
+static mp_status head_t(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
+  const int s = c->cfg.s, h = c->cfg.h, Tn = s * b, Vr = c->cfg.V / c->t;
+  const int ie = c->param_index.at("emb#-1"), ig = c->param_index.at("lnf_g#-1"), ib = c->param_index.at("lnf_b#-1");
+  const size_t es = c->esz;
+  size_t o_Z = 0, o_mu = o_Z + al256(es * Tn * h), o_rs = o_mu + al256(4ull * Tn), o_L = o_rs + al256(4ull * Tn),
+         o_dL = o_L + al256(4ull * Tn * Vr), o_mx = o_dL + al256(es * Tn * Vr), o_st = o_mx + al256(4ull * Tn),
+         o_dZ = o_st + al256(8ull * Tn), tot = o_dZ + al256(es * Tn * h);
+  void* blk = nullptr;
+  MP_TRY(alloc_async(c, &blk, tot, c->cs));
+  char* base = (char*)blk;
+  T* Z = (T*)(base + o_Z);
+  float *mu = (float*)(base + o_mu), *rs = (float*)(base + o_rs), *L = (float*)(base + o_L);
+  T* dL = (T*)(base + o_dL);
+  float *mx = (float*)(base + o_mx), *stt = (float*)(base + o_st);
+  T* dZ = (T*)(base + o_dZ);
+  MP_TRY(layernorm_fwd<T>((const T*)X, ptr<T>(c, ig), ptr<T>(c, ib), Z, mu, rs, Tn, h, c->cfg.ln_eps, c->cs));
+  {  // logits = Z E_r^T  (fp32 out)
+    mp_gemm_desc g{};
+    g.M = Tn; g.N = Vr; g.K = h; g.batch = 1;
+    g.A = Z; g.lda = h; g.B = ptr<T>(c, ie); g.ldb = h; g.C = L; g.ldc = Vr; g.c_fp32 = 1; g.alpha = 1.f;
+    MP_TRY(gemm(c->cfg.dtype, g, c->cs));
+  }
+  MP_TRY(ce_rowmax(L, mx, Tn, Vr, c->cs));
+  if (c->t > 1) MP_TRY(nccl_check(ncclAllReduce(mx, mx, Tn, ncclFloat32, ncclMax, c->tp_comm, c->cs), "ce max"));
+  MP_TRY(ce_sumexp_target(L, mx, dlab, lab_ld, s, b, c->tp * Vr, stt, Tn, Vr, c->cs));
+  if (c->t > 1) MP_TRY(nccl_check(ncclAllReduce(stt, stt, 2 * Tn, ncclFloat32, ncclSum, c->tp_comm, c->cs), "ce sum"));
+  MP_TRY(ce_loss_grad<T>(L, mx, stt, dlab, lab_ld, s, b, c->tp * Vr, scale, dL, c->d_loss, Tn, Vr, c->cs));
+  {  // dZ = dlogits E_r
+    mp_gemm_desc g{};
+    g.M = Tn; g.N = h; g.K = Vr; g.batch = 1;
+    g.A = dL; g.lda = Vr; g.B = ptr<T>(c, ie); g.ldb = h; g.b_major = 1; g.C = dZ; g.ldc = h; g.alpha = 1.f;
+    g.c_fp32 = c->cfg.dtype == MP_FP32;
+    MP_TRY(gemm(c->cfg.dtype, g, c->cs));
+  }
+  MP_TRY(allreduce(c, dZ, (size_t)Tn * h, c->cs));                              // f
+  {  // dE_r += dlogits^T Z
+    mp_gemm_desc g{};
+    g.M = Vr; g.N = h; g.K = Tn; g.batch = 1;
+    g.A = dL; g.lda = Vr; g.a_major = 1; g.B = Z; g.ldb = h; g.b_major = 1;
+    g.C = gptr(c, ie); g.ldc = h; g.c_fp32 = 1; g.accumulate = 1; g.alpha = 1.f;
+    MP_TRY(gemm(c->cfg.dtype, g, c->cs));
+  }
+  MP_TRY(layernorm_bwd<T>(dZ, (const T*)X, ptr<T>(c, ig), mu, rs, nullptr, (T*)dX,
+                          gptr(c, ig), gptr(c, ib), c->ws_ln, Tn, h, c->cs));
+  MP_CUDA(cudaFreeAsync(blk, c->cs));
+  return MP_OK;
+}
+
+mp_status head_fwd_bwd(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
+  MP_TRY(ensure_workspace(c, b));
+  return c->cfg.dtype == MP_BF16 ? head_t<__nv_bfloat16>(c, X, dlab, lab_ld, b, scale, dX)
+                                 : head_t<float>(c, X, dlab, lab_ld, b, scale, dX);
+}
+
+}  // namespace mp

@@ -1,0 +1,17 @@
+// Layer / model-end building blocks used by the runtime (layer.cu).
+#pragma once
+#include "runtime.h"
+
+namespace mp {
+
+mp_status nccl_check(ncclResult_t r, const char* what);
+mp_status alloc_async(mp_ctx* c, void** p, size_t bytes, cudaStream_t st);
+mp_status ensure_workspace(mp_ctx* c, int b);
+mp_status layer_fwd(mp_ctx* c, int layer, int b, const void* x, void* y, LayerStash& st);
+mp_status layer_bwd(mp_ctx* c, int layer, const LayerStash& st, const void* dy, void* dx);
+mp_status stash_release(mp_ctx* c, LayerStash& st, cudaStream_t s);
+mp_status embed_forward(mp_ctx* c, const int* dtok, int tok_ld, int b, void* X);
+mp_status embed_backward(mp_ctx* c, const int* dtok, int tok_ld, int b, const void* dX);
+mp_status head_fwd_bwd(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX);
+
+}  // namespace mp

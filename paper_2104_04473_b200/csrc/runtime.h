@@ -1,0 +1,87 @@
+// Per-process runtime state of the PTD-P hot path: process grid, NCCL
+// communicators, weight shards, gradient accumulators, Adam state,
+// activation stash and workspaces.
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/mp.h"
+#include "schedule.h"
+
+namespace mp {
+
+// One parameter tensor of this rank, inside the flat parameter arrays.
+// Weight matrices are stored transposed w.r.t. the math orientation
+// (row = output feature, contiguous = input feature: "K-major" for the
+// forward GEMM), e.g. W_qkv shard [3h/t, h].
+struct Param {
+  std::string name;
+  int layer;           // -1 for model-level parameters
+  long long off;       // element offset in the flat arrays
+  long long numel;
+  int rows, cols;      // storage shape
+};
+
+struct LayerParams {
+  int idx[12];         // indices into ctx->params for ln1_g .. b_2
+};
+
+// Activations stashed by one layer forward for its backward.
+struct LayerStash {
+  void* x = nullptr;   // layer input [T, h]
+  bool own_x = false;  // freed with the stash
+  void* block = nullptr;  // single allocation holding everything below
+  float *mu1, *rs1, *mu2, *rs2;
+  void *A, *QKV, *P, *ctx, *X1, *A2, *Y1, *H;
+  int b = 1;
+};
+
+struct HeadStash {
+  void* block = nullptr;
+};
+
+}  // namespace mp
+
+struct mp_ctx {
+  // process grid, rank = (dp * p + pp) * t + tp
+  int t, p, v, d, rank, world, tp, pp, device;
+  mp_model_cfg cfg;
+  int esz;                       // storage element size
+  ncclDataType_t nccl_dt;
+  // communicators
+  ncclComm_t world_comm = nullptr, tp_comm = nullptr, emb_comm = nullptr;
+  ncclComm_t act_send = nullptr, act_recv = nullptr, grad_send = nullptr, grad_recv = nullptr;
+  // streams
+  cudaStream_t cs = nullptr, side = nullptr, s_act_send = nullptr, s_act_recv = nullptr, s_grad_send = nullptr,
+               s_grad_recv = nullptr;
+  cudaMemPool_t pool = nullptr;
+  // stage map
+  std::vector<int> dev_of_layer, chunk_of_layer;
+  bool has_emb = false, has_head = false;   // stage 0 / stage S-1 on this device
+  // parameters (flat)
+  std::vector<mp::Param> params;
+  std::map<std::string, int> param_index;   // "name#layer" -> index
+  std::map<int, mp::LayerParams> layer_params;
+  long long n_params = 0;
+  float* master = nullptr;     // fp32 master weights
+  void* wstore = nullptr;      // storage copy (bf16) or == master (fp32)
+  float* grads = nullptr;
+  float* adam_m = nullptr;
+  float* adam_v = nullptr;
+  long long adam_step = 0;
+  // stash slots of mp_layer_fwd
+  std::map<int, mp::LayerStash> slots;
+  int next_slot = 1;
+  // workspaces (sized for b = max_b)
+  int ws_b = 0;
+  void *ws_z = nullptr, *ws_dsq = nullptr, *ws_d4h = nullptr, *ws_dh1 = nullptr, *ws_dh2 = nullptr,
+       *ws_dqkv = nullptr, *ws_dctx = nullptr;
+  float* ws_ln = nullptr;
+  float* d_loss = nullptr;
+  // events for task timing
+  std::vector<cudaEvent_t> events;
+};

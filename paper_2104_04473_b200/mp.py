@@ -80,6 +80,15 @@ SIGNATURES = {
     "mp_run_batch": (_I, [_P, _I, _I, _I, _I, _P, _I, ctypes.POINTER(_F), ctypes.POINTER(BatchStats)]),
     "mp_op_gemm": (_I, [_I, ctypes.POINTER(GemmDesc), _P]),
     "mp_op_gemm_config": (_I, [ctypes.POINTER(GemmDesc), _P]),
+    "mp_op_layernorm_fwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P]),
+    "mp_op_bda_layernorm_fwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P]),
+    "mp_op_layernorm_bwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
+    "mp_op_layernorm_bwd_scratch_floats": (_LL, [_I, _I]),
+    "mp_op_bias_gelu_fwd": (_I, [_I, _P, _P, _P, _LL, _I, _P]),
+    "mp_op_bias_gelu_bwd": (_I, [_I, _P, _P, _P, _P, _P, _I, _I, _P]),
+    "mp_op_softmax_causal_fwd": (_I, [_I, _P, _LL, _I, _F, _P]),
+    "mp_op_softmax_causal_bwd": (_I, [_I, _P, _P, _LL, _I, _F, _P]),
+    "mp_op_colsum_accum": (_I, [_I, _P, _P, _I, _I, _P]),
 }
 
 
@@ -165,8 +174,16 @@ def mp_op_gemm_config(desc):
 
 
 def call(name, *args):
-    """Generic marshalling for the mp_op_* kernel entry points."""
+    """Generic marshalling for the mp_op_* kernel entry points (dtype given as
+    'bf16' / 'fp32' in the first position)."""
+    if args and isinstance(args[0], str):
+        args = (DTYPES[args[0]],) + tuple(args[1:])
     _check(_sym(name)(*args))
+
+
+def raw(name, *args):
+    """Call an entry point that returns a value rather than an mp_status."""
+    return _sym(name)(*args)
 
 
 # ----------------------------------------------------------------- context
