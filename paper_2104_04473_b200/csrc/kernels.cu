@@ -269,8 +269,11 @@ __global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, c
     const int vi = threadIdx.x + k * blockDim.x;
     if (vi < nvec) {
       float* pg = part + (long long)blockIdx.x * 2 * h + vi * V;
-      st_vec(pg, adg[k]);
-      st_vec(pg + h, adb[k]);
+#pragma unroll
+      for (int e = 0; e < V; e += 4) {   // V fp32 partials = V/4 float4 stores
+        st_vec(pg + e, adg[k] + e);
+        st_vec(pg + h + e, adb[k] + e);
+      }
     }
   }
 }

@@ -311,7 +311,8 @@ mp_status mp_set_weights(mp_ctx* c, const char* name, int layer, const float* ho
       if (sm.transposed) st[(size_t)j * sm.math_rows + i] = val;
       else st[(size_t)i * sm.math_cols + j] = val;
     }
-  MP_CUDA(cudaMemcpy(c->master + P.off, st.data(), st.size() * 4, cudaMemcpyHostToDevice));
+  // same stream as the cast: a pageable cudaMemcpy may return before its DMA lands
+  MP_CUDA(cudaMemcpyAsync(c->master + P.off, st.data(), st.size() * 4, cudaMemcpyHostToDevice, c->cs));
   MP_TRY(cast_store(c, P.off, P.numel, c->cs));
   MP_CUDA(cudaStreamSynchronize(c->cs));
   return MP_OK;
@@ -359,7 +360,7 @@ mp_status mp_layer_fwd(mp_ctx* c, int layer, int b, const void* x, void* y, int*
   if (b < 1) return set_err(MP_EINVAL, "b must be >= 1");
   MP_CUDA(cudaSetDevice(c->device));
   cudaStream_t saved = c->cs;
-  if (stream) c->cs = reinterpret_cast<cudaStream_t>(stream);
+  c->cs = reinterpret_cast<cudaStream_t>(stream);   // NULL = legacy default stream (header contract)
   LayerStash st;
   const size_t bytes = (size_t)c->cfg.s * b * c->cfg.h * c->esz;
   mp_status s = alloc_async(c, &st.x, bytes, c->cs);
@@ -384,7 +385,7 @@ mp_status mp_layer_bwd(mp_ctx* c, int layer, int b, int slot, const void* dy, vo
   if (it->second.b != b) return set_err(MP_EINVAL, "b differs from the forward");
   MP_CUDA(cudaSetDevice(c->device));
   cudaStream_t saved = c->cs;
-  if (stream) c->cs = reinterpret_cast<cudaStream_t>(stream);
+  c->cs = reinterpret_cast<cudaStream_t>(stream);   // NULL = legacy default stream
   mp_status s = layer_bwd(c, layer, it->second, dy, dx);
   if (s == MP_OK) s = stash_release(c, it->second, c->cs);
   c->cs = saved;

@@ -52,9 +52,8 @@ def run_gemm(M, N, K, z, am, bm, dtype="bf16", c_fp32=False, bias=False, accumul
     ref = gemm_ref(A, Bm, alpha, bvec) + (C0 if accumulate else 0)
     got = host(dC)
     if causal == 1:
-        rows = np.arange(M)[:, None] // 128
-        cols = np.arange(N)[None, :]
-        keep = cols <= rows * 128 + 127
+        # only the causal part j <= i is defined (P:312 implicit causal mask)
+        keep = np.arange(N)[None, :] <= np.arange(M)[:, None]
         ref = np.where(keep[None], ref, 0.0)
         got = np.where(keep[None], got, 0.0)
     return got, ref
@@ -94,3 +93,51 @@ def test_gemm_fp32(am, bm, causal):
     else:
         got, ref = run_gemm(200, 136, 72, 2, am, bm, dtype="fp32", causal=causal, bias=True, accumulate=True)
     assert normwise(got, ref) < 1e-5
+
+
+@pytest.mark.parametrize("am,bm", [(0, 0), (0, 1), (1, 0), (1, 1)])
+@pytest.mark.parametrize("M,N,K", [(512, 64, 32), (64, 512, 16), (256, 256, 8), (32, 96, 64), (512, 64, 48)])
+def test_gemm_bf16_short_k(am, bm, M, N, K):
+    """Reductions shorter than one 64-wide k-block (TMA zero-fills the rest):
+    the dE = dlogits^T Z GEMM of the tiny model has K = T = 32."""
+    got, ref = run_gemm(M, N, K, 1, am, bm, c_fp32=True)
+    assert normwise(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("s,b,heads,hd", [(256, 2, 4, 64), (128, 3, 2, 96), (32, 1, 2, 16), (256, 1, 4, 64)])
+def test_gemm_attention_layout(dtype, s, b, heads, hd):
+    """Scores S = Q K^T and context P V straight from the [s, b, heads, 3, hd]
+    QKV layout (strided batched over b*heads, no transposes)."""
+    QKV = gen.activations((s, b, heads, 3, hd), 31, 1.0, dtype)
+    q = dev(QKV, dtype)
+    z = b * heads
+    ldq = b * heads * 3 * hd
+    S = torch.zeros((z, s, s), dtype=torch.float32, device="cuda")
+    d = mp.GemmDesc()
+    d.M, d.N, d.K, d.batch = s, s, hd, z
+    d.A, d.lda, d.strideA = q.data_ptr(), ldq, 3 * hd
+    d.B, d.ldb, d.strideB = q.data_ptr() + hd * q.element_size(), ldq, 3 * hd
+    d.C, d.ldc, d.strideC = S.data_ptr(), s, s * s
+    d.c_fp32, d.alpha = 1, 1.0
+    mp.mp_op_gemm(dtype, d)
+    P = gen.activations((z, s, s), 32, 1.0, dtype)
+    Pd = dev(P, dtype)
+    ctx = torch.zeros((s, b, heads, hd), dtype=torch.float32, device="cuda")
+    e = mp.GemmDesc()
+    e.M, e.N, e.K, e.batch = s, hd, s, z
+    e.A, e.lda, e.strideA = Pd.data_ptr(), s, s * s
+    e.B, e.ldb, e.strideB = q.data_ptr() + 2 * hd * q.element_size(), ldq, 3 * hd
+    e.b_major = 1
+    e.C, e.ldc, e.strideC = ctx.data_ptr(), b * heads * hd, hd
+    e.c_fp32, e.alpha = 1, 1.0
+    mp.mp_op_gemm(dtype, e)
+    torch.cuda.synchronize()
+    Q4 = QKV
+    for bb in range(b):
+        for j in range(heads):
+            zz = bb * heads + j
+            Sr = Q4[:, bb, j, 0] @ Q4[:, bb, j, 1].T
+            assert normwise(host(S[zz]), Sr) < 1e-4, (bb, j)
+            Cr = P[zz] @ Q4[:, bb, j, 2]
+            assert normwise(host(ctx[:, bb, j]), Cr) < 1e-4, (bb, j)

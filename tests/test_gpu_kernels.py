@@ -27,16 +27,16 @@ def test_layernorm_fwd_bwd(dtype, R, h):
     dres = gen.activations((R, h), 4, 1.0, dtype)
     dx_, y_ = dev(np.zeros((R, h)), dtype), dev(np.zeros((R, h)), dtype)
     mu, rs = f32(R), f32(R)
-    mp.call("mp_op_layernorm_fwd", dtype, dev(x, dtype).data_ptr(), dev(g, dtype).data_ptr(),
-            dev(b, dtype).data_ptr(), y_.data_ptr(), mu.data_ptr(), rs.data_ptr(), R, h, 1e-5, None)
+    xd, gd, bd, dyd, dresd = (dev(a, dtype) for a in (x, g, b, dy, dres))   # keep device buffers alive
+    mp.call("mp_op_layernorm_fwd", dtype, xd.data_ptr(), gd.data_ptr(), bd.data_ptr(), y_.data_ptr(),
+            mu.data_ptr(), rs.data_ptr(), R, h, 1e-5, None)
     yr, cache = L.ln_fwd(x, g, b)
     torch.cuda.synchronize()
     assert normwise(host(y_), yr) < TOL[dtype] / 4
     dg, db = f32(h), f32(h)
     scratch = f32(mp.raw("mp_op_layernorm_bwd_scratch_floats", R, h))
-    xd, gd = dev(x, dtype), dev(g, dtype)
-    mp.call("mp_op_layernorm_bwd", dtype, dev(dy, dtype).data_ptr(), xd.data_ptr(), gd.data_ptr(), mu.data_ptr(),
-            rs.data_ptr(), dev(dres, dtype).data_ptr(), dx_.data_ptr(), dg.data_ptr(), db.data_ptr(),
+    mp.call("mp_op_layernorm_bwd", dtype, dyd.data_ptr(), xd.data_ptr(), gd.data_ptr(), mu.data_ptr(),
+            rs.data_ptr(), dresd.data_ptr(), dx_.data_ptr(), dg.data_ptr(), db.data_ptr(),
             scratch.data_ptr(), R, h, None)
     torch.cuda.synchronize()
     dxr, dgr, dbr = L.ln_bwd(dy, cache, g)
@@ -66,7 +66,8 @@ def test_softmax_causal(dtype, z, s):
     dP = gen.activations((z, s, s), 6, 1.0, dtype)
     Pd = gen.round_to(Pr, dtype)          # the kernel consumes the stored P
     dbuf = dev(dP, dtype)
-    mp.call("mp_op_softmax_causal_bwd", dtype, dbuf.data_ptr(), dev(Pd, dtype).data_ptr(), z, s, float(scale), None)
+    Pdd = dev(Pd, dtype)
+    mp.call("mp_op_softmax_causal_bwd", dtype, dbuf.data_ptr(), Pdd.data_ptr(), z, s, float(scale), None)
     torch.cuda.synchronize()
     dS = host(dbuf)
     dSr = L.softmax_bwd(np.where(j <= i, dP, 0), Pd) * scale

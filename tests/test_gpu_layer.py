@@ -81,7 +81,8 @@ def test_layer_paper_width_1_7b(dtype):
         xd, yd = dev(X, dtype), dev(np.zeros_like(X), dtype)
         slot = ctx.layer_fwd(0, 1, xd.data_ptr(), yd.data_ptr())
         dxd = dev(np.zeros_like(X), dtype)
-        ctx.layer_bwd(0, 1, slot, dev(dY, dtype).data_ptr(), dxd.data_ptr())
+        dyd = dev(dY, dtype)
+        ctx.layer_bwd(0, 1, slot, dyd.data_ptr(), dxd.data_ptr())
         torch.cuda.synchronize()
         Yr, cache = L.layer_fwd(X, W, shape.a)
         dXr, gr = L.layer_bwd(dY, cache, W, shape.a)
