@@ -97,6 +97,28 @@ def layer_weights(h, l_total, seed, layer, dtype="bf16"):
             for k, shp in layer_param_shapes(h).items()}
 
 
+def _draw32(rng, name, shape, l):
+    x = rng.standard_normal(shape, dtype=np.float32)
+    if name.endswith("_g"):
+        return 1.0 + 0.1 * x
+    if name in ("w_o", "w_2"):
+        return np.float32(0.02 / np.sqrt(2.0 * l)) * x
+    return np.float32(0.02) * x
+
+
+def layer_weights_fast(h, l_total, seed, layer):
+    """Same recipe drawn directly in float32 (large benchmark models; the
+    library rounds to its storage dtype).  Not used for parity tests."""
+    rng = np.random.Generator(np.random.PCG64([seed, 1, layer]))
+    return {k: _draw32(rng, k, shp, l_total) for k, shp in layer_param_shapes(h).items()}
+
+
+def model_weights_fast(cfg, seed=42):
+    """Model-level tensors (emb, pos, lnf_*) of the fast float32 recipe."""
+    rng = np.random.Generator(np.random.PCG64([seed, 0]))
+    return {k: _draw32(rng, k, shp, cfg.l) for k, shp in model_param_shapes(cfg).items()}
+
+
 def model_weights(cfg, seed=42, dtype="bf16"):
     """All weights of a GPT model: {'layers': [dict per layer], 'emb', 'pos', 'lnf_g', 'lnf_b'}."""
     rng = np.random.Generator(np.random.PCG64([seed, 0]))

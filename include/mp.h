@@ -177,6 +177,19 @@ mp_status mp_layer_bwd(mp_ctx* ctx, int layer, int b, int stash_slot, const void
 mp_status mp_run_batch(mp_ctx* ctx, int B, int b, int m, mp_schedule sched, const int* tokens,
                        int apply_optimizer, float* loss_out, mp_batch_stats* stats);
 
+/* The library's compute stream for this context (cudaStream_t as void*): the
+ * stream every forward/backward task of mp_run_batch* is issued on, so that
+ * callers can bracket batches with CUDA events on it. */
+void* mp_compute_stream(mp_ctx* ctx);
+
+/* mp_run_batch with the inputs already resident in device memory: d_tokens
+ * device int32 [B, s+1]; the mean loss is written (stream-ordered) to the
+ * device float *d_loss.  No host synchronisation unless stats != NULL.  Used
+ * to time the path without host<->device copies; semantics otherwise equal
+ * to mp_run_batch. */
+mp_status mp_run_batch_dev(mp_ctx* ctx, int B, int b, int m, mp_schedule sched, const int* d_tokens,
+                           int apply_optimizer, float* d_loss, mp_batch_stats* stats);
+
 #ifdef __cplusplus
 }
 #endif

@@ -59,6 +59,21 @@ mp_status mp_op_gemm(mp_dtype dtype, const mp_gemm_desc* g, void* stream);
  * out[0] = BN, out[1] = stages, out[2] = grid size. */
 mp_status mp_op_gemm_config(const mp_gemm_desc* g, int* out3);
 
+/* Algorithmic FLOPs of a GEMM call: 2 M N K batch, or for the causal modes
+ * only the defined lower-triangular part (Appendix P:574 counts 2Bs^2h per
+ * attention product; the causal kernels never execute the upper half). */
+double mp_gemm_flops(const mp_gemm_desc* g);
+
+/* Live GEMM profile: while enabled, every bf16 GEMM launch is bracketed by
+ * CUDA events on its own stream.  mp_profile_gemm(1) enables and resets,
+ * (0) disables; mp_profile_gemm_read synchronises the device and returns the
+ * summed algorithmic FLOPs, summed kernel seconds and the launch count. */
+mp_status mp_profile_gemm(int enable);
+mp_status mp_profile_gemm_read(double* flops, double* seconds, long long* launches);
+
+/* Number of kernels launched by this library since it was loaded. */
+long long mp_launch_count(void);
+
 /* LayerNorm over rows of x [R, h] (implied by Eq. (1)'s 13h term, P:344;
  * pre-LN GPT layer, reading #1; biased variance, eps): y = g * xhat + b;
  * per-row fp32 mean / rstd saved for the backward.  h <= 8192 (bf16). */

@@ -12,6 +12,9 @@ mp_status set_err(mp_status s, const char* fmt, ...);
 int num_sms();
 // MP_OK if an sm_100 device is current, else MP_ECUDA (no CPU fallback exists).
 mp_status require_device();
+// Count of kernels this library has launched (bench bookkeeping).
+void count_launch(int n = 1);
+long long launch_count();
 
 }  // namespace mp
 

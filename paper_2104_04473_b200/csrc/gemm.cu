@@ -21,6 +21,8 @@
 #include <cstdio>
 #include <cstring>
 #include <mutex>
+#include <vector>
+#include <algorithm>
 
 #include "ptx.cuh"
 #include "common.h"
@@ -414,8 +416,45 @@ mp_status gemm_fp32(const mp_gemm_desc& g, cudaStream_t st) {
   return MP_OK;
 }
 
+// ------------------------------------------------------ live GEMM profile
+// Algorithmic FLOPs of one call: 2 M N K per batch for dense GEMMs; for the
+// causal attention GEMMs only the defined (lower-triangular) part counts, the
+// upper triangle being work the method avoids.
+double gemm_algorithmic_flops(const mp_gemm_desc& g) {
+  double rows = 0;
+  if (g.causal == 0) return 2.0 * g.M * (double)g.N * g.K * g.batch;
+  for (int i = 0; i < g.M; ++i) {
+    if (g.causal == 1) rows += std::min(g.N, i + 1);
+    else if (g.causal == 2) rows += std::min(g.K, i + 1);
+    else rows += std::max(0, g.K - i);
+  }
+  return 2.0 * rows * (g.causal == 1 ? g.K : g.N) * g.batch;
+}
+
+struct ProfRec { cudaEvent_t a, b; double flops; };
+static bool g_prof = false;
+static std::vector<ProfRec> g_recs;
+static std::vector<cudaEvent_t> g_evpool;
+static size_t g_evnext = 0;
+static cudaEvent_t prof_event() {
+  if (g_evnext == g_evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_evpool.push_back(e);
+  }
+  return g_evpool[g_evnext++];
+}
+
 mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st) {
-  return dt == MP_BF16 ? gemm_bf16(g, st) : gemm_fp32(g, st);
+  if (dt != MP_BF16) { count_launch(); return gemm_fp32(g, st); }
+  count_launch();
+  if (!g_prof) return gemm_bf16(g, st);
+  ProfRec r{prof_event(), prof_event(), gemm_algorithmic_flops(g)};
+  cudaEventRecord(r.a, st);
+  mp_status s = gemm_bf16(g, st);
+  cudaEventRecord(r.b, st);
+  g_recs.push_back(r);
+  return s;
 }
 
 }  // namespace mp
@@ -425,6 +464,29 @@ extern "C" mp_status mp_op_gemm(mp_dtype dtype, const mp_gemm_desc* g, void* str
   MP_REQUIRE_DEVICE();
   return mp::gemm(dtype, *g, reinterpret_cast<cudaStream_t>(stream));
 }
+
+extern "C" mp_status mp_profile_gemm(int enable) {
+  mp::g_prof = enable != 0;
+  mp::g_recs.clear();
+  mp::g_evnext = 0;
+  return MP_OK;
+}
+
+extern "C" mp_status mp_profile_gemm_read(double* flops, double* seconds, long long* launches) {
+  if (!flops || !seconds || !launches) return mp::set_err(MP_EINVAL, "null arg");
+  MP_CUDA(cudaDeviceSynchronize());
+  double f = 0, t = 0;
+  for (auto& r : mp::g_recs) {
+    float ms = 0.f;
+    MP_CUDA(cudaEventElapsedTime(&ms, r.a, r.b));
+    f += r.flops;
+    t += ms * 1e-3;
+  }
+  *flops = f; *seconds = t; *launches = (long long)mp::g_recs.size();
+  return MP_OK;
+}
+
+extern "C" double mp_gemm_flops(const mp_gemm_desc* g) { return g ? mp::gemm_algorithmic_flops(*g) : 0.0; }
 
 extern "C" mp_status mp_op_gemm_config(const mp_gemm_desc* g, int* out3) {
   if (!g || !out3) return mp::set_err(MP_EINVAL, "null arg");

@@ -3,6 +3,7 @@
 // work without a GPU), except the device query helpers at the bottom.
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -14,6 +15,10 @@
 namespace mp {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+
+void count_launch(int n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 mp_status set_err(mp_status s, const char* fmt, ...) {
   va_list ap;
@@ -98,6 +103,8 @@ using namespace mp;
 extern "C" {
 
 const char* mp_last_error(void) { return g_err; }
+
+long long mp_launch_count(void) { return launch_count(); }
 
 double mp_flops(long long B, long long s, long long l, long long h, long long V, int recompute) {
   // Eq. (2); sum of the Appendix terms in exact integers

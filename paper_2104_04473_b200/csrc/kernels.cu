@@ -81,6 +81,7 @@ constexpr int LN_MAXV = 4;
 
 #define LAUNCH_CHECK()                                                                         \
   do {                                                                                         \
+    count_launch();                                                                            \
     cudaError_t _e = cudaGetLastError();                                                       \
     if (_e != cudaSuccess) return set_err(MP_ECUDA, "%s: %s", __func__, cudaGetErrorString(_e)); \
     return MP_OK;                                                                              \
@@ -342,6 +343,7 @@ mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, 
     // dgamma: rows of stride 2h starting at scratch; dbeta at scratch + h
     colsum_strided_kernel<<<grid, bx, 0, st>>>(scratch, dgamma, nb, h, 2LL * h);
     colsum_strided_kernel<<<grid, bx, 0, st>>>(scratch + h, dbeta, nb, h, 2LL * h);
+    count_launch(2);
   }
   LAUNCH_CHECK();
 }

@@ -394,9 +394,9 @@ mp_status mp_layer_bwd(mp_ctx* c, int layer, int b, int slot, const void* dy, vo
 }
 
 // ------------------------------------------------------------- batch call
-mp_status mp_run_batch(mp_ctx* c, int B, int b, int m, mp_schedule sched, const int* tokens, int apply_optimizer,
-                       float* loss_out, mp_batch_stats* stats) {
-  if (!c || !tokens || !loss_out) return set_err(MP_EINVAL, "null argument");
+static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sched, const int* tokens, bool tok_dev,
+                                int apply_optimizer, float* loss_host, float* loss_dev, mp_batch_stats* stats) {
+  if (!c || !tokens || (!loss_host && !loss_dev)) return set_err(MP_EINVAL, "null argument");
   if (b < 1 || m < 1 || B != m * b * c->d) return set_err(MP_EDIV, "need B = m b d (P:189): B=%d b=%d m=%d", B, b, m);
   if ((sched == MP_GPIPE || sched == MP_1F1B) && c->v != 1)
     return set_err(MP_ESCHED, "context built with v=%d needs the interleaved schedule", c->v);
@@ -417,8 +417,12 @@ mp_status mp_run_batch(mp_ctx* c, int B, int b, int m, mp_schedule sched, const 
   MP_CUDA(cudaEventRecord(ev_start, cs));
   // tokens -> device (inputs x = tok[:, :s], labels y = tok[:, 1:])
   int* dtok = nullptr;
-  MP_TRY(alloc_async(c, (void**)&dtok, sizeof(int) * (size_t)B * (s + 1), cs));
-  MP_CUDA(cudaMemcpyAsync(dtok, tokens, sizeof(int) * (size_t)B * (s + 1), cudaMemcpyHostToDevice, cs));
+  if (tok_dev) {
+    dtok = const_cast<int*>(tokens);
+  } else {
+    MP_TRY(alloc_async(c, (void**)&dtok, sizeof(int) * (size_t)B * (s + 1), cs));
+    MP_CUDA(cudaMemcpyAsync(dtok, tokens, sizeof(int) * (size_t)B * (s + 1), cudaMemcpyHostToDevice, cs));
+  }
   MP_CUDA(cudaMemsetAsync(c->grads, 0, (size_t)c->n_params * 4, cs));
   MP_CUDA(cudaMemsetAsync(c->d_loss, 0, 4, cs));
 
@@ -562,12 +566,14 @@ mp_status mp_run_batch(mp_ctx* c, int B, int b, int m, mp_schedule sched, const 
       MP_TRY(adam_step<float>(c->master, c->grads, c->adam_m, c->adam_v, c->master, c->n_params, c->cfg.lr, b1, b2,
                               1e-8f, bc1, bc2, cs));
   }
-  MP_CUDA(cudaFreeAsync(dtok, cs));
+  if (!tok_dev) MP_CUDA(cudaFreeAsync(dtok, cs));
+  if (loss_host) {
+    MP_CUDA(cudaMemcpyAsync(loss_host, c->d_loss + 32, 4, cudaMemcpyDeviceToHost, cs));
+  } else {
+    MP_CUDA(cudaMemcpyAsync(loss_dev, c->d_loss + 32, 4, cudaMemcpyDeviceToDevice, cs));
+  }
   MP_CUDA(cudaEventRecord(ev_end, cs));
-  float loss = 0.f;
-  MP_CUDA(cudaMemcpyAsync(&loss, c->d_loss + 32, 4, cudaMemcpyDeviceToHost, cs));
-  MP_CUDA(cudaStreamSynchronize(cs));
-  *loss_out = loss;
+  if (loss_host || stats) MP_CUDA(cudaStreamSynchronize(cs));
   if (!stash.empty() || !local_act.empty() || !local_grad.empty())
     return set_err(MP_ESTATE, "pipeline finished with live activations (schedule bug)");
   if (stats) {
@@ -590,6 +596,18 @@ mp_status mp_run_batch(mp_ctx* c, int B, int b, int m, mp_schedule sched, const 
   }
   (void)st;
   return MP_OK;
+}
+
+mp_status mp_run_batch(mp_ctx* c, int B, int b, int m, mp_schedule sched, const int* tokens, int apply_optimizer,
+                       float* loss_out, mp_batch_stats* stats) {
+  return run_batch_impl(c, B, b, m, sched, tokens, false, apply_optimizer, loss_out, nullptr, stats);
+}
+
+void* mp_compute_stream(mp_ctx* c) { return c ? reinterpret_cast<void*>(c->cs) : nullptr; }
+
+mp_status mp_run_batch_dev(mp_ctx* c, int B, int b, int m, mp_schedule sched, const int* d_tokens,
+                           int apply_optimizer, float* d_loss, mp_batch_stats* stats) {
+  return run_batch_impl(c, B, b, m, sched, d_tokens, true, apply_optimizer, nullptr, d_loss, stats);
 }
 
 }  // extern "C"

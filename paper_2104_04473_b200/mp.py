@@ -78,7 +78,13 @@ SIGNATURES = {
     "mp_layer_fwd": (_I, [_P, _I, _I, _P, _P, ctypes.POINTER(_I), _P]),
     "mp_layer_bwd": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "mp_run_batch": (_I, [_P, _I, _I, _I, _I, _P, _I, ctypes.POINTER(_F), ctypes.POINTER(BatchStats)]),
+    "mp_compute_stream": (_P, [_P]),
+    "mp_run_batch_dev": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, ctypes.POINTER(BatchStats)]),
     "mp_op_gemm": (_I, [_I, ctypes.POINTER(GemmDesc), _P]),
+    "mp_gemm_flops": (_D, [ctypes.POINTER(GemmDesc)]),
+    "mp_profile_gemm": (_I, [_I]),
+    "mp_profile_gemm_read": (_I, [ctypes.POINTER(_D), ctypes.POINTER(_D), ctypes.POINTER(_LL)]),
+    "mp_launch_count": (_LL, []),
     "mp_op_gemm_config": (_I, [ctypes.POINTER(GemmDesc), _P]),
     "mp_op_layernorm_fwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P]),
     "mp_op_bda_layernorm_fwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P]),
@@ -231,10 +237,39 @@ class Context:
     def layer_bwd(self, layer, b, slot, dy_ptr, dx_ptr, stream=0):
         _check(_sym("mp_layer_bwd")(self.ptr, layer, b, slot, dy_ptr, dx_ptr, stream))
 
-    def run_batch(self, B, b, m, sched, tokens, apply_optimizer=False):
-        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+    def run_batch(self, B, b, m, sched, tokens, apply_optimizer=False, stats=True):
+        """tokens: numpy int32 [B, s+1] or an integer host address (e.g. pinned memory)."""
+        if isinstance(tokens, int):
+            addr = tokens
+        else:
+            tok = np.ascontiguousarray(tokens, dtype=np.int32)
+            addr = tok.ctypes.data
         loss = _F(0.0)
         st = BatchStats()
-        _check(_sym("mp_run_batch")(self.ptr, B, b, m, SCHEDULES[sched], tok.ctypes.data, int(apply_optimizer),
-                                    ctypes.byref(loss), ctypes.byref(st)))
-        return loss.value, st.as_dict()
+        _check(_sym("mp_run_batch")(self.ptr, B, b, m, SCHEDULES[sched], addr, int(apply_optimizer),
+                                    ctypes.byref(loss), ctypes.byref(st) if stats else None))
+        return loss.value, (st.as_dict() if stats else None)
+
+    def stream(self):
+        return _sym("mp_compute_stream")(self.ptr)
+
+    def run_batch_dev(self, B, b, m, sched, d_tokens, d_loss, apply_optimizer=False, stats=False):
+        """Device-resident variant: d_tokens / d_loss are device addresses."""
+        st = BatchStats()
+        _check(_sym("mp_run_batch_dev")(self.ptr, B, b, m, SCHEDULES[sched], d_tokens, int(apply_optimizer), d_loss,
+                                        ctypes.byref(st) if stats else None))
+        return st.as_dict() if stats else None
+
+
+def profile_gemm(enable):
+    _check(_sym("mp_profile_gemm")(int(enable)))
+
+
+def profile_gemm_read():
+    f, t, n = _D(0), _D(0), _LL(0)
+    _check(_sym("mp_profile_gemm_read")(ctypes.byref(f), ctypes.byref(t), ctypes.byref(n)))
+    return f.value, t.value, n.value
+
+
+def launch_count():
+    return _sym("mp_launch_count")()
