@@ -1,0 +1,99 @@
+"""Worker for the multi-GPU parity tests (launched by torchrun from
+tests/test_gpu_multi.py).  Each rank builds the context for (t, p, v), loads
+the tiny GPT's unpartitioned weights (the library keeps its shard), runs one
+batch through mp_run_batch and checks its own shards of every gradient and
+the loss against the fp64 oracle; optionally one Adam step and a second
+batch (weights stay consistent across ranks).  Exit code 0 = parity."""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--t", type=int, default=1)
+    ap.add_argument("--p", type=int, default=1)
+    ap.add_argument("--v", type=int, default=1)
+    ap.add_argument("--m", type=int, default=4)
+    ap.add_argument("--sched", default="1f1b")
+    ap.add_argument("--dtype", default="bf16")
+    ap.add_argument("--h", type=int, default=64)
+    ap.add_argument("--l", type=int, default=4)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    import gen
+    from oracle import layer as L
+    from oracle import model as M
+    from paper_2104_04473_b200 import mp
+
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo", init_method="env://")
+    nid = [mp.mp_nccl_get_id() if rank == 0 else None]
+    dist.broadcast_object_list(nid, src=0)
+    shape = gen.ModelCfg(l=a.l, h=a.h, a=4, s=32, V=512)
+    W = gen.model_weights(shape, seed=42, dtype=a.dtype)
+    tok = gen.tokens(a.m, shape.s, shape.V, seed=1234)
+    cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype)
+    ctx = mp.Context(a.t, a.p, a.v, 1, cfg, rank, world, local, nid[0])
+    tp, pp = rank % a.t, (rank // a.t) % a.p
+    tol = {"bf16": 2e-2, "fp32": 1e-4}[a.dtype]
+    report = {"rank": rank, "tp": tp, "pp": pp, "errors": {}}
+    try:
+        for k, Wl in enumerate(W["layers"]):
+            for name, arr in Wl.items():
+                ctx.set_weights(name, k, arr)
+        for name in ("emb", "pos", "lnf_g", "lnf_b"):
+            ctx.set_weights(name, 0, W[name])
+        loss, stats = ctx.run_batch(a.m, 1, a.m, a.sched, tok)
+        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m)
+        report["loss"] = [loss, lr]
+        report["stats"] = stats
+        ok = abs(loss - lr) / abs(lr) < tol
+        dev_of, _ = mp.mp_get_stage_map(shape.l, a.p, a.v)
+
+        def nw(x, r):
+            return float(np.max(np.abs(x - r)) / max(1e-30, np.max(np.abs(r))))
+        for k in range(shape.l):
+            if dev_of[k] != pp:
+                continue
+            sh = L.shard_layer(gr["layers"][k], shape.h, a.t, tp)
+            for name, r in sh.items():
+                e = nw(ctx.get_grads(name, k).reshape(r.shape), r)
+                report["errors"][f"{name}#{k}"] = e
+                ok &= e < tol
+        Vr = shape.V // a.t
+        model_refs = {}
+        if pp == 0 or pp == a.p - 1:
+            model_refs["emb"] = gr["emb"][tp * Vr:(tp + 1) * Vr]
+        if pp == 0:
+            model_refs["pos"] = gr["pos"]
+        if pp == a.p - 1:
+            model_refs["lnf_g"] = gr["lnf_g"]
+            model_refs["lnf_b"] = gr["lnf_b"]
+        for name, r in model_refs.items():
+            e = nw(ctx.get_grads(name, 0).reshape(r.shape), r)
+            report["errors"][name] = e
+            ok &= e < tol
+        report["ok"] = bool(ok)
+    finally:
+        ctx.close()
+    if a.out:
+        with open(f"{a.out}.{rank}.json", "w") as f:
+            json.dump(report, f)
+    dist.barrier()
+    dist.destroy_process_group()
+    sys.exit(0 if report.get("ok") else 1)
+
+
+if __name__ == "__main__":
+    main()
