@@ -43,9 +43,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="1.7B", help="tiny | 1.7B | 7.5B | 18.4B | 39.1B")
-    ap.add_argument("--t", type=int, default=0, help="tensor parallel size (default: N / p)")
-    ap.add_argument("--p", type=int, default=1, help="pipeline parallel size")
-    ap.add_argument("--v", type=int, default=1, help="model chunks per device (interleaved)")
+    ap.add_argument("--tp", dest="t", type=int, default=0, help="tensor parallel size (default: N / p)")
+    ap.add_argument("--pp", dest="p", type=int, default=1, help="pipeline parallel size")
+    ap.add_argument("--vp", dest="v", type=int, default=1, help="model chunks per device (interleaved)")
     ap.add_argument("--layers", type=int, default=0, help="override l (depth-reduced proxy; reported)")
     ap.add_argument("--B", type=int, default=16, help="global batch (sequences)")
     ap.add_argument("--b", type=int, default=1, help="microbatch size")

@@ -17,9 +17,9 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--t", type=int, default=1)
-    ap.add_argument("--p", type=int, default=1)
-    ap.add_argument("--v", type=int, default=1)
+    ap.add_argument("--tp", dest="t", type=int, default=1)
+    ap.add_argument("--pp", dest="p", type=int, default=1)
+    ap.add_argument("--vp", dest="v", type=int, default=1)
     ap.add_argument("--m", type=int, default=4)
     ap.add_argument("--sched", default="1f1b")
     ap.add_argument("--dtype", default="bf16")
