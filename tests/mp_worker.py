@@ -26,7 +26,9 @@ def main():
     ap.add_argument("--h", type=int, default=64)
     ap.add_argument("--l", type=int, default=4)
     ap.add_argument("--out", default="")
-    a = ap.parse_args()
+    # arguments come through MP_WORKER_ARGS: torchrun's own parser would
+    # otherwise claim any option that prefixes one of its flags (--m, --t ...)
+    a = ap.parse_args(os.environ.get("MP_WORKER_ARGS", "").split())
     import torch
     import torch.distributed as dist
 

@@ -42,9 +42,9 @@ def test_multi_gpu_parity(tmp_path, t, p, v, m, sched, dtype):
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={29500 + (hash((t, p, v, m, sched, dtype)) % 2000)}",
-           os.path.join(ROOT, "tests", "mp_worker.py"), "--tp", str(t), "--pp", str(p), "--vp", str(v),
-           "--m", str(m), "--sched", sched, "--dtype", dtype, "--out", out]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype {dtype} --out {out}")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
     msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
     assert r.returncode == 0, msg
