@@ -18,6 +18,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -163,6 +165,14 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
   if (cfg->p_drop_attn != 0.f || cfg->p_drop_hidden != 0.f)
     return set_err(MP_EUNSUPPORTED, "dropout p > 0 is not built in this round (DESIGN.md)");
   if (cfg->dtype != MP_BF16 && cfg->dtype != MP_FP32) return set_err(MP_EINVAL, "bad dtype");
+  if (p > 1) {
+    // Six library streams (+ the caller's): fewer hardware queues create
+    // false dependencies between a compute-stream wait and a channel's NCCL
+    // kernel, which deadlocks the pipeline.
+    const char* mc = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
+    if (mc && atoi(mc) < 8)
+      return set_err(MP_EINVAL, "CUDA_DEVICE_MAX_CONNECTIONS=%s is too small for p > 1 (need >= 8, use 32)", mc);
+  }
   MP_CUDA(cudaSetDevice(local_device));
   MP_REQUIRE_DEVICE();
   mp_ctx* c = new mp_ctx();
@@ -185,6 +195,12 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
   MP_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, local_device));
   uint64_t thr = UINT64_MAX;
   MP_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  if (getenv("MP_POOL_NOREUSE")) {
+    int zero = 0;
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseFollowEventDependencies, &zero);
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowOpportunistic, &zero);
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+  }
   for (int i = 0; i < 2; ++i) {
     cudaEvent_t e;
     MP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -201,35 +217,8 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
     if (r != ncclSuccess) return set_err(MP_ENCCL, "tp split: %s", ncclGetErrorString(r));
   }
   if (p > 1) {
-    // Directed ring edges e_r: r -> r+1 (activations) and r+1 -> r (gradients).
-    // Edges are split into rounds so that no rank is in two edges of a round:
-    // color(e_r) = r % 2, and 2 for the closing edge of an odd ring.
-    auto color = [&](int e) { return (p % 2 == 1 && e == p - 1) ? 2 : e % 2; };
-    const int rounds = p % 2 ? 3 : 2;
-    for (int kind = 0; kind < 2; ++kind) {      // 0 = activations, 1 = gradients
-      for (int k = 0; k < rounds; ++k) {
-        int col = NCCL_SPLIT_NOCOLOR, keyv = 0;
-        int edge_src = -1;                       // edge index if this rank takes part
-        for (int e = 0; e < p; ++e) {
-          if (color(e) != k) continue;
-          const int a = e, b = (e + 1) % p;        // edge between devices a and b
-          if (c->pp == a || c->pp == b) {
-            edge_src = e;
-            const int src = kind == 0 ? a : b;
-            col = e * t + c->tp;
-            keyv = c->pp == src ? 0 : 1;
-          }
-        }
-        ncclComm_t comm = nullptr;
-        r = ncclCommSplit(c->world_comm, col, keyv, &comm, nullptr);
-        if (r != ncclSuccess) return set_err(MP_ENCCL, "p2p split: %s", ncclGetErrorString(r));
-        if (edge_src < 0) continue;
-        const bool sender = keyv == 0;
-        if (kind == 0) (sender ? c->act_send : c->act_recv) = comm;
-        else (sender ? c->grad_send : c->grad_recv) = comm;
-      }
-    }
-    // p == 2: both edges join the same two devices but are separate comms.
+    // tied word embedding: stage 0 and stage S-1 hold copies of E_r (pipeline
+    // activations / gradients travel over the IPC channels of p2p.cu)
     const bool tie = c->pp == 0 || c->pp == p - 1;
     r = ncclCommSplit(c->world_comm, tie ? c->tp : NCCL_SPLIT_NOCOLOR, c->pp == 0 ? 0 : 1, &c->emb_comm, nullptr);
     if (r != ncclSuccess) return set_err(MP_ENCCL, "embedding split: %s", ncclGetErrorString(r));
@@ -278,7 +267,8 @@ mp_status mp_finalize(mp_ctx* c) {
   cudaDeviceSynchronize();
   for (auto& kv : c->slots) stash_release(c, kv.second, c->cs);
   cudaStreamSynchronize(c->cs);
-  ncclComm_t comms[] = {c->tp_comm, c->emb_comm, c->act_send, c->act_recv, c->grad_send, c->grad_recv, c->world_comm};
+  p2p_release(c);
+  ncclComm_t comms[] = {c->tp_comm, c->emb_comm, c->world_comm};
   for (auto cm : comms)
     if (cm) ncclCommDestroy(cm);
   void* bufs[] = {c->ws_z, c->ws_dsq, c->ws_d4h, c->ws_dh1, c->ws_dh2, c->ws_dqkv, c->ws_dctx, c->ws_ln,
@@ -413,6 +403,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   const float scale = 1.f / ((float)B * (float)s);
   cudaStream_t cs = c->cs;
 
+  MP_TRY(p2p_ensure(c, act_bytes));
   cudaEvent_t ev_start = X.timing.get(), ev_end = X.timing.get();
   MP_CUDA(cudaEventRecord(ev_start, cs));
   // tokens -> device (inputs x = tok[:, :s], labels y = tok[:, 1:])
@@ -432,8 +423,11 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   int inflight = 0, peak = 0;
   mp_status st = MP_OK;
 
+  static const bool dbg = getenv("MP_DEBUG") != nullptr;
   for (const Task& tk : tasks) {
     const int sigma = tk.chunk * p + c->pp;
+    if (dbg) fprintf(stderr, "[mp rank %d] enqueue %c mb=%d chunk=%d stage=%d\n", c->rank, tk.kind ? 'B' : 'F', tk.mb,
+                     tk.chunk, sigma);
     const int* tok = dtok + (size_t)tk.mb * b * (s + 1);
     if (tk.kind == 0) {
       // ------------------------------------------------------------ forward
@@ -445,7 +439,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
         local_act.erase({tk.mb, sigma});
       } else {
         MP_TRY(alloc_async(c, &x, act_bytes, c->s_act_recv));
-        MP_TRY(nccl_check(ncclRecv(x, act_elems, c->nccl_dt, 0, c->act_recv, c->s_act_recv), "recv act"));
+        MP_TRY(p2p_recv_act(c, x, act_bytes, c->s_act_recv));
         cudaEvent_t e = X.sync.get();
         MP_CUDA(cudaEventRecord(e, c->s_act_recv));
         MP_CUDA(cudaStreamWaitEvent(cs, e, 0));
@@ -477,10 +471,14 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
       } else {
         MP_CUDA(cudaEventRecord(t1, cs));
         MP_CUDA(cudaStreamWaitEvent(c->s_act_send, t1, 0));
-        MP_TRY(nccl_check(ncclSend(x, act_elems, c->nccl_dt, 1, c->act_send, c->s_act_send), "send act"));
+        MP_TRY(p2p_send_act(c, x, act_bytes, c->s_act_send));
         MP_CUDA(cudaFreeAsync(x, c->s_act_send));
       }
       task_ev.push_back({t0, t1});
+      if (dbg && getenv("MP_DEBUG")[0] == '2') {
+        cudaError_t e2 = cudaStreamSynchronize(cs);
+        fprintf(stderr, "[mp rank %d] done F mb=%d (%s)\n", c->rank, tk.mb, cudaGetErrorString(e2));
+      }
     } else {
       // ----------------------------------------------------------- backward
       void* dy = nullptr;
@@ -489,7 +487,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
         local_grad.erase({tk.mb, sigma});
       } else {
         MP_TRY(alloc_async(c, &dy, act_bytes, c->s_grad_recv));
-        MP_TRY(nccl_check(ncclRecv(dy, act_elems, c->nccl_dt, 0, c->grad_recv, c->s_grad_recv), "recv grad"));
+        MP_TRY(p2p_recv_grad(c, dy, act_bytes, c->s_grad_recv));
         cudaEvent_t e = X.sync.get();
         MP_CUDA(cudaEventRecord(e, c->s_grad_recv));
         MP_CUDA(cudaStreamWaitEvent(cs, e, 0));
@@ -517,13 +515,18 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
       } else {
         MP_CUDA(cudaEventRecord(t1, cs));
         MP_CUDA(cudaStreamWaitEvent(c->s_grad_send, t1, 0));
-        MP_TRY(nccl_check(ncclSend(dy, act_elems, c->nccl_dt, 1, c->grad_send, c->s_grad_send), "send grad"));
+        MP_TRY(p2p_send_grad(c, dy, act_bytes, c->s_grad_send));
         MP_CUDA(cudaFreeAsync(dy, c->s_grad_send));
       }
       task_ev.push_back({t0, t1});
+      if (dbg && getenv("MP_DEBUG")[0] == '2') {
+        cudaError_t e2 = cudaStreamSynchronize(cs);
+        fprintf(stderr, "[mp rank %d] done B mb=%d (%s)\n", c->rank, tk.mb, cudaGetErrorString(e2));
+      }
     }
   }
   // ------------------------------------------------------------------ flush
+  if (dbg) fprintf(stderr, "[mp rank %d] all tasks enqueued\n", c->rank);
   if (p > 1) {
     cudaStream_t ss[] = {c->s_act_send, c->s_grad_send, c->s_act_recv, c->s_grad_recv};
     for (auto q : ss) {

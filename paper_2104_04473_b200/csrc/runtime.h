@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "../../include/mp.h"
+#include "p2p.h"
 #include "schedule.h"
 
 namespace mp {
@@ -54,7 +55,6 @@ struct mp_ctx {
   ncclDataType_t nccl_dt;
   // communicators
   ncclComm_t world_comm = nullptr, tp_comm = nullptr, emb_comm = nullptr;
-  ncclComm_t act_send = nullptr, act_recv = nullptr, grad_send = nullptr, grad_recv = nullptr;
   // streams
   cudaStream_t cs = nullptr, side = nullptr, s_act_send = nullptr, s_act_recv = nullptr, s_grad_send = nullptr,
                s_grad_recv = nullptr;
@@ -84,4 +84,6 @@ struct mp_ctx {
   float* d_loss = nullptr;
   // events for task timing
   std::vector<cudaEvent_t> events;
+  // pipeline channels (p > 1)
+  mp::P2PRing p2p;
 };

@@ -11,6 +11,14 @@ import os
 
 import numpy as np
 
+# The pipeline runtime uses one compute stream, one side stream and four P2P
+# channel streams per process.  With fewer hardware work queues than streams,
+# a stream-wait on a P2P event can block a channel's NCCL kernel queued behind
+# it (false dependency -> deadlock), so ask for the maximum before CUDA
+# initialises in this process.  mp_init refuses p > 1 when the setting is
+# too small.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libmp.so")
 

@@ -11,6 +11,11 @@ import sys
 
 import numpy as np
 
+# Enough hardware work queues that the compute stream's waits on P2P events
+# never sit in front of a channel stream's NCCL kernel (false dependencies
+# deadlock the pipeline otherwise).  Must be set before CUDA initialises.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
