@@ -211,11 +211,10 @@ def main():
     B, b = args.B, args.b
     m = B // b
     # ---- context (NCCL id from rank 0, broadcast by the launcher)
-    nid = [mp.mp_nccl_get_id() if rank == 0 else None]
-    if world > 1:
-        dist.broadcast_object_list(nid, src=0)
+    from paper_2104_04473_b200 import launch
+    nid = launch.share_bytes(mp.mp_nccl_get_id() if rank == 0 else None, rank, world)
     c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5)
-    ctx = mp.Context(t, p, v, 1, c, rank, world, local, nid[0])
+    ctx = mp.Context(t, p, v, 1, c, rank, world, local, nid)
     # ---- random-init weights (only the owned shards are kept)
     dev_of, _ = mp.mp_get_stage_map(cfg.l, p, v)
     pp = (rank // t) % p
@@ -262,10 +261,7 @@ def main():
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     t_step = ms / 1e3 / args.steps
-    if world > 1:
-        tt = torch.tensor([t_step], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step = float(tt.item())
+    t_step = launch.max_over_ranks(t_step, world, "cuda")
     loss_val = float(d_loss.item())
     # ---- end to end through the public API: pinned host tokens in, loss out, every step
     e2e = None
@@ -279,10 +275,7 @@ def main():
             ctx.run_batch(B, b, m, sched, pinned.data_ptr(), apply_optimizer=True, stats=False)
         torch.cuda.synchronize()
         w = (time.perf_counter() - w0) / args.steps
-        if world > 1:
-            tt = torch.tensor([w], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            w = float(tt.item())
+        w = launch.max_over_ranks(w, world, "cuda")
         e2e = {"value": F / w / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(tok.nbytes),
                "d2h_bytes_per_step": 4, "ms_per_step": 1e3 * w,
                "how": "mp_run_batch with pinned host tokens (H2D inside) and the loss read back every step; "
