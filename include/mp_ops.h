@@ -87,8 +87,8 @@ mp_status mp_op_bda_layernorm_fwd(mp_dtype dt, const void* y, const void* bias, 
                                   float eps, void* stream);
 
 /* LayerNorm backward: dx = LN'(dy) (+ dres if non-NULL); dgamma, dbeta
- * (fp32 [h]) are ACCUMULATED (+=).  scratch: fp32 workspace of
- * mp_op_layernorm_bwd_scratch_floats(R, h) floats. */
+ * (fp32 [h]) are ACCUMULATED (+=).  scratch is unused (may be NULL);
+ * mp_op_layernorm_bwd_scratch_floats returns 0 and is kept for ABI stability. */
 mp_status mp_op_layernorm_bwd(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
                               const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
                               float* scratch, int R, int h, void* stream);

@@ -42,7 +42,9 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  // epilogue staging: per epilogue warp two 32-row x 128-byte boxes (TMA store)
+  static constexpr int STAGE_OUT_BYTES = EPI_WARPS * 2 * 4096;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT_BYTES + 1024 + 256;
 };
 
 struct TcArgs {
@@ -52,6 +54,7 @@ struct TcArgs {
   long long ldc, strideC;
   const __nv_bfloat16* bias;
   int c_fp32, accumulate, causal, vec_ok;
+  int tma_out;          // epilogue through shared memory + TMA store / reduce-add (tmC valid)
   float alpha;
 };
 
@@ -68,14 +71,16 @@ __device__ __forceinline__ void k_range(const TcArgs& g, int m_blk, int& kb0, in
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcArgs g) {
+tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, TcArgs g) {
   using Cfg = TcCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* sOut = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sOut + Cfg::STAGE_OUT_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -89,7 +94,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    if (g.tma_out) tma_prefetch(&tmC);
+  }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -171,6 +180,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // -------------------------------------------------- epilogue
     const int quarter = warp % 4;            // TMEM lanes 32*quarter .. +31
     int acc = 0; uint32_t acc_phase = 0;
+    int obuf = 0;                            // staging buffer (double buffered per warp)
+    uint8_t* stage_base = sOut + (warp - 2) * 2 * 4096;
     for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
       const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
       const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
@@ -179,57 +190,97 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const bool have_acc = kb1 > kb0;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * BM + quarter * 32 + lane;
-      const bool row_ok = row < g.M;
-      for (int c0 = 0; c0 < BN; c0 += 32) {
-        const int col0 = n_blk * BN + c0;
-        if (col0 >= g.N) break;
-        uint32_t r[32];
-        tmem_ld_32x32b_x32(tmem_base + acc * BN + c0 + ((uint32_t)(quarter * 32) << 16), r);
-        tmem_ld_wait();
-        if (!row_ok) continue;
-        float v[32];
+      const int row0 = m_blk * BM + quarter * 32;
+      const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      if (g.tma_out) {
+        // TMEM -> registers -> 128B-swizzled staging box (32 rows x 128 B) -> TMA
+        // store (bf16 / fp32) or TMA reduce-add (fp32 gradient accumulation).
+        const int cw = g.c_fp32 ? 32 : 64;     // 128-byte rows: 32 fp32 or 64 bf16 columns per box
+        for (int c0 = 0; c0 < BN; c0 += cw) {
+          const int col0 = n_blk * BN + c0;
+          if (col0 >= g.N) break;
+          // the staging buffer written two boxes ago must have been read by its TMA
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint8_t* buf = stage_base + obuf * 4096;
+          const uint32_t rowaddr = smem_u32(buf) + lane * 128;
+          if (g.c_fp32) {
+            uint32_t r[32];
+            tmem_ld_32x32b_x32(tbase + c0, r);
+            tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = have_acc ? __uint_as_float(r[j]) * g.alpha : 0.f;
-        const int ncols = min(32, g.N - col0);
-        if (g.bias) {
+            for (int j = 0; j < 8; ++j) {
+              float v[4];
 #pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < ncols) v[j] += __bfloat162float(g.bias[col0 + j]);
-        }
-        const long long off = (long long)z * g.strideC + (long long)row * g.ldc + col0;
-        if (g.c_fp32) {
-          float* C = reinterpret_cast<float*>(g.C) + off;
-          if (g.vec_ok && ncols == 32) {
-#pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              float4 o = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-              if (g.accumulate) {
-                float4 c = *reinterpret_cast<const float4*>(C + j);
-                o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
+              for (int e = 0; e < 4; ++e) {
+                const int c = 4 * j + e;
+                v[e] = have_acc ? __uint_as_float(r[c]) * g.alpha : 0.f;
+                if (g.bias && col0 + c < g.N) v[e] += __bfloat162float(g.bias[col0 + c]);
               }
-              *reinterpret_cast<float4*>(C + j) = o;
+              st_shared_v4(rowaddr + ((j ^ (lane & 7)) << 4), __float_as_uint(v[0]), __float_as_uint(v[1]),
+                           __float_as_uint(v[2]), __float_as_uint(v[3]));
             }
           } else {
-            for (int j = 0; j < ncols; ++j) C[j] = g.accumulate ? C[j] + v[j] : v[j];
-          }
-        } else {
-          __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(g.C) + off;
-          if (g.vec_ok && ncols == 32) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              uint4 o;
-              __nv_bfloat162 p0 = __floats2bfloat162_rn(v[j], v[j + 1]);
-              __nv_bfloat162 p1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-              __nv_bfloat162 p2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]);
-              __nv_bfloat162 p3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-              o.x = *reinterpret_cast<uint32_t*>(&p0);
-              o.y = *reinterpret_cast<uint32_t*>(&p1);
-              o.z = *reinterpret_cast<uint32_t*>(&p2);
-              o.w = *reinterpret_cast<uint32_t*>(&p3);
-              *reinterpret_cast<uint4*>(C + j) = o;
+            for (int hf = 0; hf < 2; ++hf) {
+              uint32_t r[32];
+              tmem_ld_32x32b_x32(tbase + c0 + 32 * hf, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                uint32_t w[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const int c = 8 * j + 2 * e;
+                  float a0 = have_acc ? __uint_as_float(r[c]) * g.alpha : 0.f;
+                  float a1 = have_acc ? __uint_as_float(r[c + 1]) * g.alpha : 0.f;
+                  const int gc = col0 + 32 * hf + c;
+                  if (g.bias) {
+                    if (gc < g.N) a0 += __bfloat162float(g.bias[gc]);
+                    if (gc + 1 < g.N) a1 += __bfloat162float(g.bias[gc + 1]);
+                  }
+                  __nv_bfloat162 pr = __floats2bfloat162_rn(a0, a1);
+                  w[e] = *reinterpret_cast<uint32_t*>(&pr);
+                }
+                const int chunk = 4 * hf + j;
+                st_shared_v4(rowaddr + ((chunk ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
+              }
             }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (g.accumulate) tma_reduce_add_3d(&tmC, buf, col0, row0, z);
+            else tma_store_3d(&tmC, buf, col0, row0, z);
+            bulk_commit();
+          }
+          obuf ^= 1;
+        }
+      } else {
+        const int row = row0 + lane;
+        const bool row_ok = row < g.M;
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          const int col0 = n_blk * BN + c0;
+          if (col0 >= g.N) break;
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tbase + c0, r);
+          tmem_ld_wait();
+          if (!row_ok) continue;
+          float v[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = have_acc ? __uint_as_float(r[j]) * g.alpha : 0.f;
+          const int ncols = min(32, g.N - col0);
+          if (g.bias) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (j < ncols) v[j] += __bfloat162float(g.bias[col0 + j]);
+          }
+          const long long off = (long long)z * g.strideC + (long long)row * g.ldc + col0;
+          if (g.c_fp32) {
+            float* C = reinterpret_cast<float*>(g.C) + off;
+            for (int j = 0; j < ncols; ++j) C[j] = g.accumulate ? C[j] + v[j] : v[j];
           } else {
+            __nv_bfloat16* C = reinterpret_cast<__nv_bfloat16*>(g.C) + off;
             for (int j = 0; j < ncols; ++j) C[j] = __float2bfloat16_rn(v[j]);
           }
         }
@@ -238,6 +289,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -323,19 +375,19 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 3-D bf16 tensor map: dims (inner, outer, batch), 128B swizzle, box (64, box_outer, 1).
+// 3-D tensor map: dims (inner, outer, batch), 128B swizzle, box (128 B of inner, box_outer, 1).
 static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t batch,
-                     uint64_t ld_elems, uint64_t batch_stride_elems, uint32_t box_outer) {
+                     uint64_t ld_elems, uint64_t batch_stride_elems, uint32_t box_outer, int esize = 2) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   if (batch <= 1) { batch = 1; batch_stride_elems = ld_elems * outer; }
   cuuint64_t dims[3] = {inner, outer, batch};
-  cuuint64_t strides[2] = {ld_elems * 2, batch_stride_elems * 2};
-  cuuint32_t box[3] = {64, box_outer, 1};
+  cuuint64_t strides[2] = {ld_elems * esize, batch_stride_elems * esize};
+  cuuint32_t box[3] = {(cuuint32_t)(128 / esize), box_outer, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(m, esize == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                  const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
@@ -349,8 +401,8 @@ static int pick_bn(const mp_gemm_desc& g) {
 }
 
 template <int BN, bool A_MN, bool B_MN>
-static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const TcArgs& a, int grid,
-                             cudaStream_t st) {
+static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const TcArgs& a,
+                             int grid, cudaStream_t st) {
   using Cfg = TcCfg<BN>;
   auto k = tc_gemm_kernel<BN, A_MN, B_MN>;
   static bool attr = false;
@@ -359,17 +411,17 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, a);
+  k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, a);
   return cudaGetLastError();
 }
 
 template <int BN>
-static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, const TcArgs& a, int grid,
-                                  int am, int bm, cudaStream_t st) {
-  if (!am && !bm) return launch_tc<BN, false, false>(ta, tb, a, grid, st);
-  if (!am && bm) return launch_tc<BN, false, true>(ta, tb, a, grid, st);
-  if (am && !bm) return launch_tc<BN, true, false>(ta, tb, a, grid, st);
-  return launch_tc<BN, true, true>(ta, tb, a, grid, st);
+static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                                  const TcArgs& a, int grid, int am, int bm, cudaStream_t st) {
+  if (!am && !bm) return launch_tc<BN, false, false>(ta, tb, tc, a, grid, st);
+  if (!am && bm) return launch_tc<BN, false, true>(ta, tb, tc, a, grid, st);
+  if (am && !bm) return launch_tc<BN, true, false>(ta, tb, tc, a, grid, st);
+  return launch_tc<BN, true, true>(ta, tb, tc, a, grid, st);
 }
 
 static int tc_grid(const TcArgs& a) { return std::max(1, std::min(a.num_tiles, num_sms())); }
@@ -398,11 +450,15 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   a.c_fp32 = g.c_fp32; a.accumulate = g.accumulate; a.causal = g.causal; a.alpha = g.alpha;
   const int esz = g.c_fp32 ? 4 : 2;
   a.vec_ok = al16(g.C) && (g.ldc * esz) % 16 == 0 && (g.strideC * esz) % 16 == 0;
+  CUtensorMap tc;
+  memset(&tc, 0, sizeof(tc));
+  // epilogue via TMA: C box = 32 rows x 128 bytes
+  a.tma_out = a.vec_ok && make_map(&tc, g.C, g.N, g.M, g.batch, g.ldc, g.strideC, 32, esz);
   const int grid = tc_grid(a);
   cudaError_t e;
-  if (BN == 64) e = dispatch_major<64>(ta, tb, a, grid, g.a_major, g.b_major, st);
-  else if (BN == 128) e = dispatch_major<128>(ta, tb, a, grid, g.a_major, g.b_major, st);
-  else e = dispatch_major<256>(ta, tb, a, grid, g.a_major, g.b_major, st);
+  if (BN == 64) e = dispatch_major<64>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);
+  else if (BN == 128) e = dispatch_major<128>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);
+  else e = dispatch_major<256>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);
   if (e != cudaSuccess) return set_err(MP_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
   return MP_OK;
 }

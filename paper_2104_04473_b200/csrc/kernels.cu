@@ -202,149 +202,153 @@ mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long
 }
 
 // ------------------------------------------------------------ LayerNorm bwd
-constexpr int LNB_ROWS = 16;
-
+// dx: one CTA per row (fp32 block sums of dxhat and dxhat*xhat).
 template <class T>
-__global__ void __launch_bounds__(256) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                     const T* __restrict__ g, const float* __restrict__ mean,
-                                                     const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                     T* __restrict__ dx, float* __restrict__ part, int R, int h) {
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                        const T* __restrict__ g, const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                        T* __restrict__ dx, int h) {
   constexpr int V = VW<T>::N;
   __shared__ float2 red[32];
+  const long long row = blockIdx.x;
   const int nvec = h / V;
-  float adg[LN_MAXV][V], adb[LN_MAXV][V], gg[LN_MAXV][V];
-#pragma unroll
-  for (int k = 0; k < LN_MAXV; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-#pragma unroll
-    for (int e = 0; e < V; ++e) { adg[k][e] = 0.f; adb[k][e] = 0.f; gg[k][e] = 0.f; }
-    if (vi < nvec) ld_vec(g + vi * V, gg[k]);
-  }
-  const int r0 = blockIdx.x * LNB_ROWS;
-  for (int rr = 0; rr < LNB_ROWS; ++rr) {
-    const long long row = r0 + rr;
-    if (row >= R) break;
-    const float mu = mean[row], rs = rstd[row];
-    float xh[LN_MAXV][V], dxh[LN_MAXV][V];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < LN_MAXV; ++k) {
-      const int vi = threadIdx.x + k * blockDim.x;
-      if (vi < nvec) {
-        float d[V], xv[V];
-        ld_vec(dy + row * h + vi * V, d);
-        ld_vec(x + row * h + vi * V, xv);
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          xh[k][e] = (xv[e] - mu) * rs;
-          dxh[k][e] = d[e] * gg[k][e];
-          s1 += dxh[k][e];
-          s2 += dxh[k][e] * xh[k][e];
-          adg[k][e] += d[e] * xh[k][e];
-          adb[k][e] += d[e];
-        }
-      }
-    }
-    const float2 s = block_sum2(s1, s2, red);
-    const float m1 = s.x / h, m2 = s.y / h;
-#pragma unroll
-    for (int k = 0; k < LN_MAXV; ++k) {
-      const int vi = threadIdx.x + k * blockDim.x;
-      if (vi < nvec) {
-        float o[V];
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
-        if (dres) {
-          float q[V];
-          ld_vec(dres + row * h + vi * V, q);
-#pragma unroll
-          for (int e = 0; e < V; ++e) o[e] += q[e];
-        }
-        st_vec(dx + row * h + vi * V, o);
-      }
-    }
-  }
-  // per-CTA partial column sums: part[blockIdx.x][0][h] = dgamma, [1][h] = dbeta
+  const float mu = mean[row], rs = rstd[row];
+  float xh[LN_MAXV][V], dxh[LN_MAXV][V];
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll
   for (int k = 0; k < LN_MAXV; ++k) {
     const int vi = threadIdx.x + k * blockDim.x;
     if (vi < nvec) {
-      float* pg = part + (long long)blockIdx.x * 2 * h + vi * V;
+      float d[V], xv[V], gg[V];
+      ld_vec(dy + row * h + vi * V, d);
+      ld_vec(x + row * h + vi * V, xv);
+      ld_vec(g + vi * V, gg);
 #pragma unroll
-      for (int e = 0; e < V; e += 4) {   // V fp32 partials = V/4 float4 stores
-        st_vec(pg + e, adg[k] + e);
-        st_vec(pg + h + e, adb[k] + e);
+      for (int e = 0; e < V; ++e) {
+        xh[k][e] = (xv[e] - mu) * rs;
+        dxh[k][e] = d[e] * gg[e];
+        s1 += dxh[k][e];
+        s2 += dxh[k][e] * xh[k][e];
       }
+    }
+  }
+  const float2 sm = block_sum2(s1, s2, red);
+  const float m1 = sm.x / h, m2 = sm.y / h;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float o[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
+      if (dres) {
+        float q[V];
+        ld_vec(dres + row * h + vi * V, q);
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] += q[e];
+      }
+      st_vec(dx + row * h + vi * V, o);
     }
   }
 }
 
-// out[n] += sum_r X[r, n] over a [R, N] matrix: 2-D grid (column vectors x row chunks), fp32 atomics.
-constexpr int CS_ROWS = 64;
-template <class T>
-__global__ void colsum_kernel(const T* __restrict__ X, float* __restrict__ out, int R, int N) {
-  constexpr int V = VW<T>::N;
-  const int vi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (vi * V >= N) return;
-  float acc[V] = {};
-  const int r0 = blockIdx.y * CS_ROWS, r1 = min(R, r0 + CS_ROWS);
-  for (int r = r0; r < r1; ++r) {
-    float v[V];
-    ld_vec(X + (long long)r * N + vi * V, v);
+// Column-reduction tiling shared by the bias / gamma / beta gradient kernels:
+// a CTA is CT_X column vectors x CT_Y row groups and covers CT_ROWS rows; a
+// thread accumulates its column vector over rows r0 + ty + CT_Y j, the CT_Y
+// partials are summed through shared memory and one fp32 atomic per column
+// per CTA adds the result into the gradient accumulator.
+constexpr int CT_X = 32, CT_Y = 8, CT_ROWS = 64;
+
+template <int V>
+__device__ __forceinline__ void ct_reduce_add(float (&acc)[V], float* red /* [CT_Y][CT_X][V] */, float* out,
+                                              int vi, int nv) {
+  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
 #pragma unroll
-    for (int e = 0; e < V; ++e) acc[e] += v[e];
+  for (int e = 0; e < V; ++e) red[(ty * CT_X + tx) * V + e] = acc[e];
+  __syncthreads();
+  if (ty == 0 && vi < nv) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) {
+      float sum = 0.f;
+#pragma unroll
+      for (int y = 0; y < CT_Y; ++y) sum += red[(y * CT_X + tx) * V + e];
+      atomicAdd(out + vi * V + e, sum);
+    }
   }
+}
+
+static inline dim3 ct_grid(int nv, int R) { return dim3((nv + CT_X - 1) / CT_X, (R + CT_ROWS - 1) / CT_ROWS); }
+
+// out[n] += sum_r X[r, n]
+template <class T>
+__global__ void __launch_bounds__(CT_X * CT_Y) colsum_kernel(const T* __restrict__ X, float* __restrict__ out, int R,
+                                                            int N) {
+  constexpr int V = VW<T>::N;
+  __shared__ float red[CT_Y * CT_X * V];
+  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
+  const int nv = N / V, vi = blockIdx.x * CT_X + tx;
+  const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
+  float acc[V] = {};
+  if (vi < nv) {
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += CT_Y) {
+      float v[V];
+      ld_vec(X + (long long)r * N + vi * V, v);
 #pragma unroll
-  for (int e = 0; e < V; ++e) atomicAdd(out + vi * V + e, acc[e]);
+      for (int e = 0; e < V; ++e) acc[e] += v[e];
+    }
+  }
+  ct_reduce_add<V>(acc, red, out, vi, nv);
 }
 
 template <class T>
 mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "colsum: N %% %d", V);
-  const int nv = N / V;
-  const int bx = std::min(256, (nv + 31) / 32 * 32);
-  dim3 grid((nv + bx - 1) / bx, (R + CS_ROWS - 1) / CS_ROWS);
-  colsum_kernel<T><<<grid, bx, 0, st>>>(X, out, R, N);
+  colsum_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(X, out, R, N);
   LAUNCH_CHECK();
 }
 
-
-__global__ void colsum_strided_kernel(const float* __restrict__ X, float* __restrict__ out, int R, int N,
-                                      long long ld) {
-  const int vi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (vi * 4 >= N) return;
-  float acc[4] = {};
-  const int r0 = blockIdx.y * CS_ROWS, r1 = min(R, r0 + CS_ROWS);
-  for (int r = r0; r < r1; ++r) {
-    float v[4];
-    ld_vec(X + (long long)r * ld + vi * 4, v);
+// dgamma[n] += sum_r dy[r,n] (x[r,n] - mean[r]) rstd[r];  dbeta[n] += sum_r dy[r,n]
+template <class T>
+__global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd,
+                                                               float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                               int R, int h) {
+  constexpr int V = VW<T>::N;
+  __shared__ float red[CT_Y * CT_X * V];
+  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
+  const int nv = h / V, vi = blockIdx.x * CT_X + tx;
+  const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
+  float ag[V] = {}, ab[V] = {};
+  if (vi < nv) {
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += CT_Y) {
+      float d[V], xv[V];
+      ld_vec(dy + (long long)r * h + vi * V, d);
+      ld_vec(x + (long long)r * h + vi * V, xv);
+      const float mu = mean[r], rs = rstd[r];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) acc[e] += v[e];
+      for (int e = 0; e < V; ++e) {
+        ag[e] += d[e] * (xv[e] - mu) * rs;
+        ab[e] += d[e];
+      }
+    }
   }
-#pragma unroll
-  for (int e = 0; e < 4; ++e) atomicAdd(out + vi * 4 + e, acc[e]);
+  ct_reduce_add<V>(ag, red, dgamma, vi, nv);
+  __syncthreads();
+  ct_reduce_add<V>(ab, red, dbeta, vi, nv);
 }
 
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
-                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st) {
+                        T* dx, float* dgamma, float* dbeta, float* /*scratch (unused)*/, int R, int h,
+                        cudaStream_t st) {
   MP_TRY(check_row_dims<T>(R, h));
-  const int nb = (R + LNB_ROWS - 1) / LNB_ROWS;
-  ln_bwd_kernel<T><<<nb, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, scratch, R, h);
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(MP_ECUDA, "ln_bwd: %s", cudaGetErrorString(e));
-  // reduce the [nb, 2, h] partials: view as nb rows of 2h columns into [dgamma | dbeta]
-  // (dgamma and dbeta are separate buffers, so reduce each half).
-  {
-    const int V = 4, nv = h / V;
-    const int bx = std::min(256, (nv + 31) / 32 * 32);
-    dim3 grid((nv + bx - 1) / bx, (nb + CS_ROWS - 1) / CS_ROWS);
-    // dgamma: rows of stride 2h starting at scratch; dbeta at scratch + h
-    colsum_strided_kernel<<<grid, bx, 0, st>>>(scratch, dgamma, nb, h, 2LL * h);
-    colsum_strided_kernel<<<grid, bx, 0, st>>>(scratch + h, dbeta, nb, h, 2LL * h);
-    count_launch(2);
-  }
+  ln_bwd_dx_kernel<T><<<R, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h);
+  count_launch();
+  ln_bwd_gb_kernel<T><<<ct_grid(h / VW<T>::N, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dgamma, dbeta, R, h);
   LAUNCH_CHECK();
 }
 
@@ -380,43 +384,46 @@ mp_status bias_gelu_fwd(const T* yv, const T* b, T* out, long long R, int N, cud
 }
 
 template <class T>
-__global__ void bias_gelu_bwd_kernel(const T* dh, const T* __restrict__ yv, const T* __restrict__ b, T* du,
-                                     float* __restrict__ db, int R, int N) {  // du may alias dh
+__global__ void __launch_bounds__(CT_X * CT_Y) bias_gelu_bwd_kernel(const T* dh, const T* __restrict__ yv,
+                                                                   const T* __restrict__ b, T* du,
+                                                                   float* __restrict__ db, int R, int N) {
+  // du may alias dh (each element is read, then written, by the same thread)
   constexpr int V = VW<T>::N;
-  const int vi = blockIdx.x * blockDim.x + threadIdx.x;
-  if (vi * V >= N) return;
-  float bb[V], acc[V] = {};
-  ld_vec(b + vi * V, bb);
-  const int r0 = blockIdx.y * CS_ROWS, r1 = min(R, r0 + CS_ROWS);
-  for (int r = r0; r < r1; ++r) {
-    float d[V], y[V];
-    const long long off = (long long)r * N + vi * V;
-    ld_vec(dh + off, d);
-    ld_vec(yv + off, y);
+  __shared__ float red[CT_Y * CT_X * V];
+  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
+  const int nv = N / V, vi = blockIdx.x * CT_X + tx;
+  const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
+  float acc[V] = {};
+  if (vi < nv) {
+    float bb[V];
+    ld_vec(b + vi * V, bb);
+#pragma unroll 2
+    for (int r = r0 + ty; r < r1; r += CT_Y) {
+      float d[V], y[V];
+      const long long off = (long long)r * N + vi * V;
+      ld_vec(dh + off, d);
+      ld_vec(yv + off, y);
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      float gd;
-      gelu_f(y[e] + bb[e], &gd);
-      d[e] *= gd;
+      for (int e = 0; e < V; ++e) {
+        float gd;
+        gelu_f(y[e] + bb[e], &gd);
+        d[e] *= gd;
+      }
+      st_vec(du + off, d);
+      // the bias gradient is the column sum of the stored (rounded) dU
+      ld_vec(du + off, d);
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] += d[e];
     }
-    st_vec(du + off, d);
-    // the bias gradient is the column sum of the stored (rounded) dU
-    ld_vec(du + off, d);
-#pragma unroll
-    for (int e = 0; e < V; ++e) acc[e] += d[e];
   }
-#pragma unroll
-  for (int e = 0; e < V; ++e) atomicAdd(db + vi * V + e, acc[e]);
+  ct_reduce_add<V>(acc, red, db, vi, nv);
 }
 
 template <class T>
 mp_status bias_gelu_bwd(const T* dh, const T* yv, const T* b, T* du, float* db, int R, int N, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "bias_gelu_bwd: N %% %d", V);
-  const int nv = N / V;
-  const int bx = std::min(256, (nv + 31) / 32 * 32);
-  dim3 grid((nv + bx - 1) / bx, (R + CS_ROWS - 1) / CS_ROWS);
-  bias_gelu_bwd_kernel<T><<<grid, bx, 0, st>>>(dh, yv, b, du, db, R, N);
+  bias_gelu_bwd_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(dh, yv, b, du, db, R, N);
   LAUNCH_CHECK();
 }
 

@@ -77,7 +77,7 @@ mp_status mp_op_layernorm_bwd(mp_dtype dt, const void* dy, const void* x, const 
   DISPATCH(dt, ln_bwd_, (dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, scratch, R, h, _st));
 }
 
-long long mp_op_layernorm_bwd_scratch_floats(int R, int h) { return (long long)((R + 15) / 16) * 2 * h; }
+long long mp_op_layernorm_bwd_scratch_floats(int R, int h) { (void)R; (void)h; return 0; }
 
 mp_status mp_op_bias_gelu_fwd(mp_dtype dt, const void* y, const void* b, void* out, long long R, int N,
                               void* stream) {
