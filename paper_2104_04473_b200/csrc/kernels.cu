@@ -428,51 +428,68 @@ mp_status bias_gelu_bwd(const T* dh, const T* yv, const T* b, T* du, float* db, 
 }
 
 // ----------------------------------------------------- causal softmax
-// One warp per row i of a [z, s, s] score tensor; the row is held in
-// registers (MAXK vectors per lane).  Reads columns j <= i only, writes
-// columns j < kend(i) (zeros for j > i).  exp2 with the scale folded into log2e.
-template <class T, int MAXK>
-__global__ void __launch_bounds__(256) softmax_fwd_kernel(T* __restrict__ S, long long rows, int s, float scale_log2) {
+// One 128-thread CTA per row i of a [z, s, s] score tensor; each thread holds
+// VPT 16-byte vectors of the row in registers (high occupancy, all loads of
+// the row in flight at once).  Reads columns j <= i only, writes columns
+// j < kend(i) (zeros for i < j < kend).  exp2 with the scale folded into log2e.
+constexpr int SM_THREADS = 128;
+
+__device__ __forceinline__ float block_max128(float a, float* red) {
+  a = warp_max(a);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = a;
+  __syncthreads();
+  const float r = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  return r;
+}
+__device__ __forceinline__ float block_sum128(float a, float* red) {
+  a = warp_sum(a);
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = a;
+  __syncthreads();
+  const float r = (red[0] + red[1]) + (red[2] + red[3]);
+  __syncthreads();
+  return r;
+}
+
+template <class T, int VPT>
+__global__ void __launch_bounds__(SM_THREADS) softmax_fwd_kernel(T* __restrict__ S, int s, float scale_log2) {
   constexpr int V = VW<T>::N;
-  const long long rg = blockIdx.x * 8LL + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (rg >= rows) return;
+  __shared__ float red[4];
+  const long long rg = blockIdx.x;
   const int i = (int)(rg % s);
   T* p = S + rg * s;
   const int nv_read = i / V + 1;
   const int nv_write = causal_kend(i, s) / V;
-  float v[MAXK][V];
+  float v[VPT][V];
   float mx = -FLT_MAX;
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    const int vi = lane + 32 * k;
+  for (int k = 0; k < VPT; ++k) {
+    const int vi = threadIdx.x + SM_THREADS * k;
     if (vi < nv_read) {
       ld_vec(p + vi * V, v[k]);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        const int col = vi * V + e;
-        v[k][e] = col <= i ? v[k][e] * scale_log2 : -FLT_MAX;
+        v[k][e] = vi * V + e <= i ? v[k][e] * scale_log2 : -FLT_MAX;
         mx = fmaxf(mx, v[k][e]);
       }
     }
   }
-  mx = warp_max(mx);
+  mx = block_max128(mx, red);
   float sum = 0.f;
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    const int vi = lane + 32 * k;
+  for (int k = 0; k < VPT; ++k) {
+    const int vi = threadIdx.x + SM_THREADS * k;
     if (vi < nv_read)
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        const int col = vi * V + e;
-        v[k][e] = col <= i ? exp2f(v[k][e] - mx) : 0.f;
+        v[k][e] = vi * V + e <= i ? exp2f(v[k][e] - mx) : 0.f;
         sum += v[k][e];
       }
   }
-  const float inv = 1.f / warp_sum(sum);
+  const float inv = 1.f / block_sum128(sum, red);
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    const int vi = lane + 32 * k;
+  for (int k = 0; k < VPT; ++k) {
+    const int vi = threadIdx.x + SM_THREADS * k;
     if (vi < nv_write) {
       float o[V];
 #pragma unroll
@@ -480,26 +497,24 @@ __global__ void __launch_bounds__(256) softmax_fwd_kernel(T* __restrict__ S, lon
       st_vec(p + vi * V, o);
     }
   }
-  // columns beyond the register window (only when s > 32*MAXK*V, never with the dispatch below)
 }
 
-template <class T, int MAXK>
-__global__ void __launch_bounds__(256) softmax_bwd_kernel(T* __restrict__ dP, const T* __restrict__ P, long long rows,
-                                                          int s, float scale) {
+template <class T, int VPT>
+__global__ void __launch_bounds__(SM_THREADS) softmax_bwd_kernel(T* __restrict__ dP, const T* __restrict__ P, int s,
+                                                                 float scale) {
   constexpr int V = VW<T>::N;
-  const long long rg = blockIdx.x * 8LL + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (rg >= rows) return;
+  __shared__ float red[4];
+  const long long rg = blockIdx.x;
   const int i = (int)(rg % s);
   T* dp = dP + rg * s;
   const T* pp = P + rg * s;
   const int nv_read = i / V + 1;
   const int nv_write = causal_kend(i, s) / V;
-  float d[MAXK][V], pv[MAXK][V];
+  float d[VPT][V], pv[VPT][V];
   float dot = 0.f;
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    const int vi = lane + 32 * k;
+  for (int k = 0; k < VPT; ++k) {
+    const int vi = threadIdx.x + SM_THREADS * k;
     if (vi < nv_read) {
       ld_vec(dp + vi * V, d[k]);
       ld_vec(pp + vi * V, pv[k]);
@@ -510,10 +525,10 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(T* __restrict__ dP, co
       }
     }
   }
-  dot = warp_sum(dot);
+  dot = block_sum128(dot, red);
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    const int vi = lane + 32 * k;
+  for (int k = 0; k < VPT; ++k) {
+    const int vi = threadIdx.x + SM_THREADS * k;
     if (vi < nv_write) {
       float o[V];
 #pragma unroll
@@ -524,10 +539,10 @@ __global__ void __launch_bounds__(256) softmax_bwd_kernel(T* __restrict__ dP, co
 }
 
 template <class T>
-static int softmax_maxk(int s) {
+static int softmax_vpt(int s) {
   constexpr int V = VW<T>::N;
-  int need = (s + 32 * V - 1) / (32 * V);
-  for (int k : {1, 2, 4, 8, 16})
+  const int need = (s / V + SM_THREADS - 1) / SM_THREADS;
+  for (int k : {1, 2, 4})
     if (k >= need) return k;
   return -1;
 }
@@ -536,18 +551,14 @@ template <class T>
 mp_status softmax_causal_fwd(T* S, long long z, int s, float scale, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (s % V) return set_err(MP_EINVAL, "softmax: s %% %d", V);
-  const int mk = softmax_maxk<T>(s);
-  if (mk < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
+  const int vpt = softmax_vpt<T>(s);
+  if (vpt < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
   const long long rows = z * s;
-  const unsigned grid = (unsigned)((rows + 7) / 8);
+  if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "softmax: too many rows");
   const float sl2 = scale * 1.4426950408889634f;
-  switch (mk) {
-    case 1: softmax_fwd_kernel<T, 1><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
-    case 2: softmax_fwd_kernel<T, 2><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
-    case 4: softmax_fwd_kernel<T, 4><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
-    case 8: softmax_fwd_kernel<T, 8><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
-    default: softmax_fwd_kernel<T, 16><<<grid, 256, 0, st>>>(S, rows, s, sl2); break;
-  }
+  if (vpt == 1) softmax_fwd_kernel<T, 1><<<(unsigned)rows, SM_THREADS, 0, st>>>(S, s, sl2);
+  else if (vpt == 2) softmax_fwd_kernel<T, 2><<<(unsigned)rows, SM_THREADS, 0, st>>>(S, s, sl2);
+  else softmax_fwd_kernel<T, 4><<<(unsigned)rows, SM_THREADS, 0, st>>>(S, s, sl2);
   LAUNCH_CHECK();
 }
 
@@ -555,17 +566,13 @@ template <class T>
 mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (s % V) return set_err(MP_EINVAL, "softmax: s %% %d", V);
-  const int mk = softmax_maxk<T>(s);
-  if (mk < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
+  const int vpt = softmax_vpt<T>(s);
+  if (vpt < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
   const long long rows = z * s;
-  const unsigned grid = (unsigned)((rows + 7) / 8);
-  switch (mk) {
-    case 1: softmax_bwd_kernel<T, 1><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
-    case 2: softmax_bwd_kernel<T, 2><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
-    case 4: softmax_bwd_kernel<T, 4><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
-    case 8: softmax_bwd_kernel<T, 8><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
-    default: softmax_bwd_kernel<T, 16><<<grid, 256, 0, st>>>(dP, P, rows, s, scale); break;
-  }
+  if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "softmax: too many rows");
+  if (vpt == 1) softmax_bwd_kernel<T, 1><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale);
+  else if (vpt == 2) softmax_bwd_kernel<T, 2><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale);
+  else softmax_bwd_kernel<T, 4><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale);
   LAUNCH_CHECK();
 }
 
