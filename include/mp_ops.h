@@ -110,6 +110,16 @@ mp_status mp_op_softmax_causal_fwd(mp_dtype dt, void* S, long long z, int s, flo
 mp_status mp_op_softmax_causal_bwd(mp_dtype dt, void* dP, const void* P, long long z, int s, float scale,
                                    void* stream);
 
+/* Fused causal attention core (same result as the
+ * scores GEMM + scale-mask-softmax + P.V GEMM of P:312 without materialising
+ * the s x s scores): qkv bf16 [s, b, heads, 3, hd] (head-major [q|k|v]),
+ * ctx bf16 [s, b, heads, hd] = softmax_causal(Q K^T / sqrt(hd)) V, and lse2
+ * fp32 [b*heads, s] = log2 sum_j exp2(log2(e) S[i,j] / sqrt(hd)) (base-2
+ * log-sum-exp of each row, kept for the backward).  hd in {32, 64, 96, 128};
+ * MP_EUNSUPPORTED otherwise.  bf16 only. */
+mp_status mp_op_flash_attn_fwd(const void* qkv, void* ctx, float* lse2, int s, int b, int heads, int hd,
+                               void* stream);
+
 /* out[n] += sum_r X[r, n] (bias gradients, fp32 out). */
 mp_status mp_op_colsum_accum(mp_dtype dt, const void* X, float* out, int R, int N, void* stream);
 

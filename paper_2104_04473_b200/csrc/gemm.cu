@@ -26,6 +26,7 @@
 
 #include "ptx.cuh"
 #include "common.h"
+#include "tma_host.h"
 #include "../../include/mp_ops.h"
 
 namespace mp {
@@ -376,8 +377,8 @@ static EncodeTiledFn encode_fn() {
 }
 
 // 3-D tensor map: dims (inner, outer, batch), 128B swizzle, box (128 B of inner, box_outer, 1).
-static bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t batch,
-                     uint64_t ld_elems, uint64_t batch_stride_elems, uint32_t box_outer, int esize = 2) {
+bool make_map(CUtensorMap* m, const void* ptr, uint64_t inner, uint64_t outer, uint64_t batch,
+              uint64_t ld_elems, uint64_t batch_stride_elems, uint32_t box_outer, int esize) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
   if (batch <= 1) { batch = 1; batch_stride_elems = ld_elems * outer; }
