@@ -120,6 +120,13 @@ mp_status mp_op_softmax_causal_bwd(mp_dtype dt, void* dP, const void* P, long lo
 mp_status mp_op_flash_attn_fwd(const void* qkv, void* ctx, float* lse2, int s, int b, int heads, int hd,
                                void* stream);
 
+/* Backward of mp_op_flash_attn_fwd: writes dQ, dK, dV into the q/k/v slots of
+ * dqkv (bf16, same layout as qkv) from qkv, ctx, dctx and lse2; ws is an fp32
+ * workspace of mp_op_flash_attn_bwd_ws_floats(s, b, heads, hd) floats. */
+long long mp_op_flash_attn_bwd_ws_floats(int s, int b, int heads, int hd);
+mp_status mp_op_flash_attn_bwd(const void* qkv, const void* ctx, const void* dctx, const float* lse2, void* dqkv,
+                               float* ws, int s, int b, int heads, int hd, void* stream);
+
 /* out[n] += sum_r X[r, n] (bias gradients, fp32 out). */
 mp_status mp_op_colsum_accum(mp_dtype dt, const void* X, float* out, int R, int N, void* stream);
 

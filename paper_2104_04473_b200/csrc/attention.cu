@@ -262,6 +262,316 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   if (warp == 1) tmem_dealloc<fa::TMEM_COLS>(tmem);
 }
 
+// ------------------------------------------------------------- backward
+// Per (head z, key/value tile j) CTA, looping over the query tiles i >= j:
+//   S = Q_i K_j^T, dP = dO_i V_j^T                       (TMEM [0,128), [128,256))
+//   P = exp2(S log2e/sqrt(hd) - L2_i), dS = P (dP - D_i) / sqrt(hd)   (compute warps)
+//   dV_j += P^T dO_i, dK_j += dS^T Q_i                   (TMEM accumulators)
+//   dQ_i  = dS K_j -> fp32 vector reductions into a dQ accumulator
+// D_i = rowsum(dO_i * O_i) is precomputed.  Q_i / dO_i / K_j tiles serve both
+// as K-major and (via the MN-major descriptor view) MN-major operands, and P
+// / dS as K-major (dQ) and MN-major (dV, dK) operands: no transposes.
+namespace fab {
+constexpr int T_BYTES = 2 * 128 * 128;       // one [128 rows x hd<=128] bf16 tile (2 hd blocks)
+constexpr int SMEM = 6 * T_BYTES + 1024 + 512;
+}  // namespace fab
+
+struct FabArgs {
+  int s, heads, hd, nq, nhb;
+  const float* L2;     // [z, s]
+  const float* D;      // [z, s]
+  float* dQacc;        // [z, s, hd] fp32 (zeroed)
+  __nv_bfloat16* dQKV; // [s, b, heads, 3, hd]
+  long long ldq;       // b * heads * 3 * hd
+  float scale_log2, scale;
+};
+
+__device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(fa::THREADS, 1)
+flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, FabArgs g) {
+  using namespace fab;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + T_BYTES;
+  uint8_t* sQ = sV + T_BYTES;
+  uint8_t* sdO = sQ + T_BYTES;
+  uint8_t* sP = sdO + T_BYTES;
+  uint8_t* sdS = sP + T_BYTES;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sdS + T_BYTES);
+  uint64_t* kv_full = bar + 0;
+  uint64_t* qd_full = bar + 1;
+  uint64_t* qd_empty = bar + 2;
+  uint64_t* sdp_full = bar + 3;
+  uint64_t* ds_ready = bar + 4;
+  uint64_t* dq_full = bar + 5;
+  uint64_t* tmem_free = bar + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int kt = (int)(blockIdx.x % g.nq);         // key/value tile
+  const int z = (int)(blockIdx.x / g.nq);
+  const int niter = g.nq - kt;                      // query tiles kt .. nq-1
+  const int tile_bytes = g.nhb * 128 * 128;
+
+  if (threadIdx.x == 0) {
+    mbar_init(kv_full, 1); mbar_init(qd_full, 1); mbar_init(qd_empty, 1); mbar_init(sdp_full, 1);
+    mbar_init(ds_ready, 128); mbar_init(dq_full, 1); mbar_init(tmem_free, 128);
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); }
+  if (warp == 1) tmem_alloc<fa::TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(kv_full, 2 * tile_bytes);
+      for (int hb = 0; hb < g.nhb; ++hb) {
+        tma_load_3d(sK + hb * 16384, &tmK, kv_full, 64 * hb, kt * 128, z);
+        tma_load_3d(sV + hb * 16384, &tmV, kv_full, 64 * hb, kt * 128, z);
+      }
+      for (int it = 0; it < niter; ++it) {
+        const int qi = kt + it;
+        if (it > 0) mbar_wait(qd_empty, (it - 1) & 1);
+        mbar_arrive_expect_tx(qd_full, 2 * tile_bytes);
+        for (int hb = 0; hb < g.nhb; ++hb) {
+          tma_load_3d(sQ + hb * 16384, &tmQ, qd_full, 64 * hb, qi * 128, z);
+          tma_load_3d(sdO + hb * 16384, &tmdO, qd_full, 64 * hb, qi * 128, z);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t id_sdp = idesc_bf16(128, 128, 0, 0);
+      const uint32_t id_dkv = idesc_bf16(128, g.hd, 1, 1);
+      const uint32_t id_dq = idesc_bf16(128, g.hd, 0, 1);
+      const int kh = g.hd / 16;
+      mbar_wait(kv_full, 0);
+      const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), adO = smem_u32(sdO);
+      const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
+      for (int it = 0; it < niter; ++it) {
+        mbar_wait(qd_full, it & 1);
+        if (it > 0) mbar_wait(tmem_free, (it - 1) & 1);
+        tc_fence_after();
+        for (int k = 0; k < kh; ++k) {       // K-major operands over hd
+          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
+          umma_f16(tmem + 0, smem_desc_sw128(aQ + off, 16, 1024), smem_desc_sw128(aK + off, 16, 1024), id_sdp,
+                   k > 0 ? 1u : 0u);
+          umma_f16(tmem + 128, smem_desc_sw128(adO + off, 16, 1024), smem_desc_sw128(aV + off, 16, 1024), id_sdp,
+                   k > 0 ? 1u : 0u);
+        }
+        umma_commit(sdp_full);
+        mbar_wait(ds_ready, it & 1);
+        tc_fence_after();
+        for (int k = 0; k < 8; ++k) {        // reductions over the 128 query rows / 128 keys
+          const uint32_t mn = k * 2048;                                  // MN-major view: K rows step
+          const uint32_t km = (k / 4) * 16384 + (k % 4) * 32;             // K-major view
+          // dV += P^T dO ; dK += dS^T Q
+          umma_f16(tmem + 256, smem_desc_sw128(aP + mn, 16384, 1024), smem_desc_sw128(adO + mn, 16384, 1024), id_dkv,
+                   (it > 0 || k > 0) ? 1u : 0u);
+          umma_f16(tmem + 384, smem_desc_sw128(adS + mn, 16384, 1024), smem_desc_sw128(aQ + mn, 16384, 1024), id_dkv,
+                   (it > 0 || k > 0) ? 1u : 0u);
+          // dQ_i = dS K  (into the dP columns, already consumed)
+          umma_f16(tmem + 128, smem_desc_sw128(adS + km, 16, 1024), smem_desc_sw128(aK + mn, 16384, 1024), id_dq,
+                   k > 0 ? 1u : 0u);
+        }
+        umma_commit(dq_full);
+        umma_commit(qd_empty);
+      }
+    }
+  } else {
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    for (int it = 0; it < niter; ++it) {
+      const int qi = kt + it;
+      const int q = qi * 128 + r;
+      const bool qok = q < g.s;
+      const float l2 = qok ? g.L2[(long long)z * g.s + q] : 0.f;
+      const float dd = qok ? g.D[(long long)z * g.s + q] : 0.f;
+      const bool diag = it == 0;
+      mbar_wait(sdp_full, it & 1);
+      tc_fence_after();
+      const uint32_t prow = smem_u32(sP) + r * 128, dsrow = smem_u32(sdS) + r * 128;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t sv[32], dv[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + 32 * c, sv);
+        tmem_ld_32x32b_x32(tmem + lane_off + 128 + 32 * c, dv);
+        tmem_ld_wait();
+        uint32_t wp[16], wd[16];
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          float p[2], ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int col = 32 * c + e + u;
+            const bool vis = qok && (!diag || col <= r);
+            p[u] = vis ? exp2f(__uint_as_float(sv[e + u]) * g.scale_log2 - l2) : 0.f;
+            ds[u] = p[u] * (__uint_as_float(dv[e + u]) - dd) * g.scale;
+          }
+          __nv_bfloat162 pp = __floats2bfloat162_rn(p[0], p[1]);
+          __nv_bfloat162 pd = __floats2bfloat162_rn(ds[0], ds[1]);
+          wp[e / 2] = *reinterpret_cast<uint32_t*>(&pp);
+          wd[e / 2] = *reinterpret_cast<uint32_t*>(&pd);
+        }
+        const uint32_t boff = (c / 2) * 16384;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int chunk = 4 * (c % 2) + u;
+          const uint32_t sw = (uint32_t)((chunk ^ (r & 7)) << 4);
+          st_shared_v4(prow + boff + sw, wp[4 * u], wp[4 * u + 1], wp[4 * u + 2], wp[4 * u + 3]);
+          st_shared_v4(dsrow + boff + sw, wd[4 * u], wd[4 * u + 1], wd[4 * u + 2], wd[4 * u + 3]);
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(ds_ready);
+      // dQ_i row -> fp32 reductions
+      mbar_wait(dq_full, it & 1);
+      tc_fence_after();
+      float* dqrow = g.dQacc + ((long long)z * g.s + q) * g.hd;
+      for (int c = 0; c < g.hd; c += 32) {
+        uint32_t v[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + 128 + c, v);
+        tmem_ld_wait();
+        if (qok) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            red_add_v4(dqrow + c + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
+                       __uint_as_float(v[e + 3]));
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tmem_free);
+    }
+    // dK_j, dV_j rows (TMEM lane = key row) -> bf16 into the K / V slots of dQKV
+    const int kvrow = kt * 128 + r;
+    if (niter > 0) {
+      // the last dq_full also covers the final dV / dK products
+      const bool ok = kvrow < g.s;
+      const int zb = z / g.heads, zh = z % g.heads;
+      (void)zb; (void)zh;
+      __nv_bfloat16* base = g.dQKV + (long long)kvrow * g.ldq + (long long)z * 3 * g.hd;
+      for (int part = 0; part < 2; ++part) {          // 0: dK (cols 384), 1: dV (cols 256)
+        const uint32_t col0 = part == 0 ? 384 : 256;
+        __nv_bfloat16* dst = base + (part == 0 ? g.hd : 2 * g.hd);
+        for (int c = 0; c < g.hd; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem + lane_off + col0 + c, v);
+          tmem_ld_wait();
+          if (ok) {
+#pragma unroll
+            for (int q4 = 0; q4 < 4; ++q4) {
+              uint4 u;
+              uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                __nv_bfloat162 pr = __floats2bfloat162_rn(__uint_as_float(v[8 * q4 + 2 * e]),
+                                                          __uint_as_float(v[8 * q4 + 2 * e + 1]));
+                w[e] = *reinterpret_cast<uint32_t*>(&pr);
+              }
+              *reinterpret_cast<uint4*>(dst + c + 8 * q4) = u;
+            }
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<fa::TMEM_COLS>(tmem);
+}
+
+// D[z, q] = sum_d dO[q, z, d] O[q, z, d]   (one warp per row)
+__global__ void flash_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
+                                     float* __restrict__ D, int s, int zn, int hd, long long ldo) {
+  const long long row = blockIdx.x * 8LL + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (row >= (long long)zn * s) return;
+  const int z = (int)(row / s), q = (int)(row % s);
+  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(dO + (long long)q * ldo + (long long)z * hd);
+  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(O + (long long)q * ldo + (long long)z * hd);
+  float acc = 0.f;
+  for (int c = lane; c < hd / 2; c += 32) {
+    const float2 x = __bfloat1622float2(a[c]), y = __bfloat1622float2(b[c]);
+    acc += x.x * y.x + x.y * y.y;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) D[row] = acc;
+}
+
+// dQacc fp32 [z, s, hd] -> bf16 Q slot of dQKV [s, b, heads, 3, hd]
+__global__ void flash_bwd_dq_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dQKV, int s, int zn,
+                                    int hd, long long ldq) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;   // one pair of elements
+  const long long n = (long long)zn * s * hd / 2;
+  if (i >= n) return;
+  const long long e = 2 * i;
+  const int d = (int)(e % hd);
+  const long long zq = e / hd;
+  const int q = (int)(zq % s), z = (int)(zq / s);
+  const float2 v = *reinterpret_cast<const float2*>(acc + e);
+  *reinterpret_cast<__nv_bfloat162*>(dQKV + (long long)q * ldq + (long long)z * 3 * hd + d) = __floats2bfloat162_rn(v.x, v.y);
+}
+
+// dQKV = d/dQKV of the fused attention, given O (= ctx), dO (= dctx), L2 from the forward.
+// workspace: fp32 [b*heads*s*hd + b*heads*s] (dQ accumulator, D).
+mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const float* L2, void* dQKV, float* ws,
+                         int s, int b, int heads, int hd, cudaStream_t st) {
+  if (hd % 32 || hd > 128 || hd < 32) return set_err(MP_EUNSUPPORTED, "flash attention needs hd in {32,64,96,128}");
+  const long long ldq = (long long)b * heads * 3 * hd, ldo = (long long)b * heads * hd;
+  const long long zn = (long long)b * heads;
+  const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(QKV);
+  CUtensorMap tq, tk, tv, tdo;
+  bool ok = make_map(&tq, q, hd, s, zn, ldq, 3LL * hd, 128) && make_map(&tk, q + hd, hd, s, zn, ldq, 3LL * hd, 128) &&
+            make_map(&tv, q + 2 * hd, hd, s, zn, ldq, 3LL * hd, 128) &&
+            make_map(&tdo, dO, hd, s, zn, ldo, (long long)hd, 128);
+  if (!ok) return set_err(MP_ECUDA, "flash attention bwd: tensor map encode failed");
+  float* dqacc = ws;
+  float* D = ws + zn * s * hd;
+  MP_CUDA(cudaMemsetAsync(dqacc, 0, sizeof(float) * zn * s * hd, st));
+  {
+    const long long rows = zn * s;
+    flash_bwd_dot_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(dO),
+                                                                   reinterpret_cast<const __nv_bfloat16*>(O), D, s,
+                                                                   (int)zn, hd, ldo);
+    count_launch();
+  }
+  FabArgs a;
+  a.s = s; a.heads = heads; a.hd = hd; a.nq = (s + 127) / 128; a.nhb = (hd + 63) / 64;
+  a.L2 = L2; a.D = D; a.dQacc = dqacc; a.dQKV = reinterpret_cast<__nv_bfloat16*>(dQKV); a.ldq = ldq;
+  a.scale = 1.f / std::sqrt((float)hd);
+  a.scale_log2 = 1.4426950408889634f * a.scale;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
+    if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd smem attr: %s", cudaGetErrorString(e));
+    attr = true;
+  }
+  flash_bwd_kernel<<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, a);
+  count_launch();
+  {
+    const long long n = zn * s * hd / 2;
+    flash_bwd_dq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dqacc, reinterpret_cast<__nv_bfloat16*>(dQKV), s,
+                                                                    (int)zn, hd, ldq);
+    count_launch();
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd launch: %s", cudaGetErrorString(e));
+  return MP_OK;
+}
+
 // QKV: [s, b, heads, 3, hd] bf16; O: [s, b, heads, hd] bf16; L2: [b*heads, s] fp32.
 mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st) {
   if (hd % 32 || hd > 128 || hd < 32) return set_err(MP_EUNSUPPORTED, "flash attention needs hd in {32,64,96,128}");
@@ -297,6 +607,16 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
 }
 
 }  // namespace mp
+
+extern "C" long long mp_op_flash_attn_bwd_ws_floats(int s, int b, int heads, int hd) {
+  return (long long)b * heads * s * (hd + 1);
+}
+
+extern "C" mp_status mp_op_flash_attn_bwd(const void* qkv, const void* ctx, const void* dctx, const float* lse2,
+                                          void* dqkv, float* ws, int s, int b, int heads, int hd, void* stream) {
+  MP_REQUIRE_DEVICE();
+  return mp::flash_attn_bwd(qkv, ctx, dctx, lse2, dqkv, ws, s, b, heads, hd, reinterpret_cast<cudaStream_t>(stream));
+}
 
 extern "C" mp_status mp_op_flash_attn_fwd(const void* qkv, void* ctx, float* lse2, int s, int b, int heads, int hd,
                                           void* stream) {

@@ -104,6 +104,8 @@ SIGNATURES = {
     "mp_op_softmax_causal_bwd": (_I, [_I, _P, _P, _LL, _I, _F, _P]),
     "mp_op_colsum_accum": (_I, [_I, _P, _P, _I, _I, _P]),
     "mp_op_flash_attn_fwd": (_I, [_P, _P, _P, _I, _I, _I, _I, _P]),
+    "mp_op_flash_attn_bwd_ws_floats": (_LL, [_I, _I, _I, _I]),
+    "mp_op_flash_attn_bwd": (_I, [_P, _P, _P, _P, _P, _P, _I, _I, _I, _I, _P]),
 }
 
 

@@ -33,3 +33,25 @@ def test_flash_fwd(s, b, heads, hd):
             l2 = (mx + np.log(np.exp(S - mx[:, None]).sum(-1))) / np.log(2)
             got = host(lse[bb * heads + j])
             assert np.max(np.abs(got - l2)) < 2e-2 * max(1.0, np.max(np.abs(l2)))
+
+
+@pytest.mark.parametrize("s,b,heads,hd", [(128, 1, 1, 64), (256, 1, 2, 128), (384, 2, 3, 96), (200, 1, 2, 64),
+                                          (2048, 1, 2, 128), (1000, 2, 2, 96), (32, 1, 2, 32)])
+def test_flash_bwd(s, b, heads, hd):
+    QKV = gen.activations((s, b, heads, 3, hd), 51, 1.0, "bf16")
+    dC = gen.activations((s, b, heads * hd), 52, 1.0, "bf16")
+    q = dev(QKV.reshape(s, b, -1), "bf16")
+    dc = dev(dC, "bf16")
+    ctx = torch.zeros((s, b, heads * hd), dtype=torch.bfloat16, device="cuda")
+    lse = torch.zeros((b * heads, s), dtype=torch.float32, device="cuda")
+    mp.call("mp_op_flash_attn_fwd", q.data_ptr(), ctx.data_ptr(), lse.data_ptr(), s, b, heads, hd, None)
+    dq = torch.zeros_like(q)
+    ws = torch.zeros(mp.raw("mp_op_flash_attn_bwd_ws_floats", s, b, heads, hd), dtype=torch.float32, device="cuda")
+    mp.call("mp_op_flash_attn_bwd", q.data_ptr(), ctx.data_ptr(), dc.data_ptr(), lse.data_ptr(), dq.data_ptr(),
+            ws.data_ptr(), s, b, heads, hd, None)
+    torch.cuda.synchronize()
+    C, Ps = L.attention_fwd(QKV.reshape(s, b, -1), heads)
+    dref = L.attention_bwd(dC, QKV.reshape(s, b, -1), Ps, heads).reshape(s, b, heads, 3, hd)
+    got = host(dq).reshape(s, b, heads, 3, hd)
+    for part, name in enumerate("QKV"):
+        assert normwise(got[..., part, :], dref[..., part, :]) < 2e-2, name
