@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--B", type=int, default=16, help="global batch (sequences)")
     ap.add_argument("--b", type=int, default=1, help="microbatch size")
     ap.add_argument("--sched", default="", help="gpipe | 1f1b | interleaved (default: 1f1b, interleaved if v > 1)")
+    ap.add_argument("--attn", default="fused", choices=["fused", "unfused"],
+                    help="attention core: fused tcgen05 flash kernel (default) or the paper's unfused "
+                         "scores GEMM + softmax + P.V GEMM")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
@@ -185,6 +188,8 @@ def workload_config(args, cfg):
             "model": f"GPT-{args.model}", "l": cfg.l, "h": cfg.h, "a": cfg.a, "seq_len": cfg.s, "V": cfg.V,
             "global_batch": args.B, "micro_batch": args.b, "m": args.B // args.b, "t": t, "p": args.p,
             "v": args.v, "d": 1, "schedule": sched, "parallelism": f"t{t}p{args.p}v{args.v}",
+            "attention": {"fused": "fused tcgen05 flash kernel (scores never materialised)",
+                          "unfused": "paper: strided-batched scores GEMM + fused causal softmax + P.V GEMM"}[args.attn],
             "l2": "working set > 126 MB L2 every step (weights alone exceed it); no flush",
             "flop_formula": "Eq. (2) 72-variant (no recomputation): 72Bslh^2(1+s/6h)+6BshV"}
 
@@ -213,7 +218,7 @@ def main():
     # ---- context (NCCL id from rank 0, broadcast by the launcher)
     from paper_2104_04473_b200 import launch
     nid = launch.share_bytes(mp.mp_nccl_get_id() if rank == 0 else None, rank, world)
-    c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5)
+    c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5, attn=args.attn)
     ctx = mp.Context(t, p, v, 1, c, rank, world, local, nid)
     # ---- random-init weights (only the owned shards are kept)
     dev_of, _ = mp.mp_get_stage_map(cfg.l, p, v)

@@ -64,6 +64,9 @@ typedef struct {
   int recompute;         /* activation recomputation; counted by mp_flops only in round 1 */
   unsigned long long seed;  /* dropout stream key */
   float lr;              /* Adam learning rate for mp_run_batch(apply_optimizer=1) */
+  int attn_impl;         /* 0: the paper's attention core -- strided-batched scores GEMM, fused
+                            scale-mask-softmax, P.V GEMM; 1: fused tcgen05 flash kernel
+                            (bf16, hd in {32,64,96,128}; otherwise falls back to 0) */
 } mp_model_cfg;
 
 /* Per-batch statistics filled by mp_run_batch. */

@@ -15,6 +15,7 @@
 //   Z   = H W2_r^T; g: all-reduce; Y = X1 + Z + b2                  (a16)
 // Backward mirrors it (a17); the two f all-reduces of the LayerNorm-input
 // gradients run on a side stream concurrently with the matching dW GEMM.
+#include <algorithm>
 #include <cmath>
 
 #include "common.h"
@@ -25,6 +26,9 @@
 namespace mp {
 
 mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st);
+mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st);
+mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const float* L2, void* dQKV, float* ws,
+                         int s, int b, int heads, int hd, cudaStream_t st);
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -82,6 +86,12 @@ static Dims dims(mp_ctx* c, int b) {
   return d;
 }
 
+// fused tcgen05 attention core usable for this configuration?
+static bool use_fused(const mp_ctx* c) {
+  const int hd = c->cfg.h / c->cfg.a;
+  return c->cfg.attn_impl == 1 && c->cfg.dtype == MP_BF16 && hd % 32 == 0 && hd >= 32 && hd <= 128;
+}
+
 mp_status alloc_async(mp_ctx* c, void** p, size_t bytes, cudaStream_t st) {
   cudaError_t e = cudaMallocFromPoolAsync(p, bytes ? bytes : 256, c->pool, st);
   if (e != cudaSuccess) return set_err(MP_ENOMEM, "device allocation of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
@@ -95,13 +105,16 @@ mp_status ensure_workspace(mp_ctx* c, int b) {
   for (void** q : bufs)
     if (*q) { cudaFree(*q); *q = nullptr; }
   if (c->ws_ln) { cudaFree(c->ws_ln); c->ws_ln = nullptr; }
+  if (c->ws_fa) { cudaFree(c->ws_fa); c->ws_fa = nullptr; }
   Dims d = dims(c, b);
+  const bool fused = use_fused(c);
   const size_t es = c->esz;
-  size_t sizes[] = {(size_t)d.T * d.h * es, (size_t)(d.z * d.sq) * es, (size_t)d.T * d.h4t * es,
+  size_t sizes[] = {(size_t)d.T * d.h * es, fused ? 256 : (size_t)(d.z * d.sq) * es, (size_t)d.T * d.h4t * es,
                     (size_t)d.T * d.h * es, (size_t)d.T * d.h * es, (size_t)d.T * d.h3t * es,
                     (size_t)d.T * d.ht * es};
   for (int i = 0; i < 7; ++i) MP_CUDA(cudaMalloc(bufs[i], al256(sizes[i])));
-  MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * mp_op_layernorm_bwd_scratch_floats(d.T, d.h))));
+  MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * std::max(1LL, mp_op_layernorm_bwd_scratch_floats(d.T, d.h)))));
+  if (fused) MP_CUDA(cudaMalloc(&c->ws_fa, al256(sizeof(float) * (size_t)d.z * d.s * (d.hd + 1))));
   c->ws_b = b;
   return MP_OK;
 }
@@ -186,7 +199,7 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
   // one block for every stashed activation of this layer
   size_t off[13], tot = 0;
   size_t sz[13] = {4ull * d.T, 4ull * d.T, 4ull * d.T, 4ull * d.T, es * d.T * d.h, es * d.T * d.h3t,
-                   es * (size_t)(d.z * d.sq), es * d.T * d.ht, es * d.T * d.h, es * d.T * d.h, es * d.T * d.h4t,
+                   use_fused(c) ? 4ull * d.z * d.s : es * (size_t)(d.z * d.sq), es * d.T * d.ht, es * d.T * d.h, es * d.T * d.h, es * d.T * d.h4t,
                    es * d.T * d.h4t, 0};
   for (int i = 0; i < 12; ++i) { off[i] = tot; tot += al256(sz[i]); }
   MP_TRY(alloc_async(c, &st.block, tot, c->cs));
@@ -201,7 +214,10 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
   MP_TRY(layernorm_fwd<T>(X, ptr<T>(c, lp[P_LN1G]), ptr<T>(c, lp[P_LN1B]), (T*)st.A, st.mu1, st.rs1, d.T, d.h, eps,
                           c->cs));
   MP_TRY(lin_fwd(c, st.A, ptr<T>(c, lp[P_WQKV]), ptr<T>(c, lp[P_BQKV]), st.QKV, d.T, d.h3t, d.h));
-  MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx));
+  if (use_fused(c))      // P holds the per-row base-2 log-sum-exp [z, s] instead of the scores
+    MP_TRY(flash_attn_fwd(st.QKV, st.ctx, (float*)st.P, d.s, d.b, d.heads, d.hd, c->cs));
+  else
+    MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx));
   MP_TRY(lin_fwd(c, st.ctx, ptr<T>(c, lp[P_WO]), nullptr, c->ws_z, d.T, d.h, d.ht));
   MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
   MP_TRY(bda_layernorm_fwd<T>((const T*)c->ws_z, ptr<T>(c, lp[P_BO]), X, (T*)st.X1, ptr<T>(c, lp[P_LN2G]),
@@ -245,7 +261,11 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   MP_TRY(colsum_accum<T>(dX1, gptr(c, lp[P_BO]), d.T, d.h, c->cs));
   MP_TRY(lin_dgrad(c, dX1, ptr<T>(c, lp[P_WO]), c->ws_dctx, d.T, d.h, d.ht));
   MP_TRY(lin_wgrad(c, dX1, st.ctx, gptr(c, lp[P_WO]), d.T, d.h, d.ht));
-  MP_TRY(attention_bwd<T>(c, d, st.QKV, st.P, c->ws_dctx, c->ws_dsq, c->ws_dqkv));
+  if (use_fused(c))
+    MP_TRY(flash_attn_bwd(st.QKV, st.ctx, c->ws_dctx, (const float*)st.P, c->ws_dqkv, c->ws_fa, d.s, d.b, d.heads,
+                          d.hd, c->cs));
+  else
+    MP_TRY(attention_bwd<T>(c, d, st.QKV, st.P, c->ws_dctx, c->ws_dsq, c->ws_dqkv));
   MP_TRY(colsum_accum<T>((const T*)c->ws_dqkv, gptr(c, lp[P_BQKV]), d.T, d.h3t, c->cs));
   T* dA = (T*)c->ws_dh1;
   MP_TRY(lin_dgrad(c, c->ws_dqkv, ptr<T>(c, lp[P_WQKV]), dA, d.T, d.h3t, d.h));

@@ -81,6 +81,7 @@ struct mp_ctx {
   void *ws_z = nullptr, *ws_dsq = nullptr, *ws_d4h = nullptr, *ws_dh1 = nullptr, *ws_dh2 = nullptr,
        *ws_dqkv = nullptr, *ws_dctx = nullptr;
   float* ws_ln = nullptr;
+  float* ws_fa = nullptr;          // fused-attention backward workspace (dQ accumulator, D)
   float* d_loss = nullptr;
   // events for task timing
   std::vector<cudaEvent_t> events;

@@ -41,7 +41,7 @@ class ModelCfg(ctypes.Structure):
     _fields_ = [("l", ctypes.c_int), ("h", ctypes.c_int), ("a", ctypes.c_int), ("s", ctypes.c_int),
                 ("V", ctypes.c_int), ("dtype", ctypes.c_int), ("p_drop_attn", ctypes.c_float),
                 ("p_drop_hidden", ctypes.c_float), ("ln_eps", ctypes.c_float), ("recompute", ctypes.c_int),
-                ("seed", ctypes.c_ulonglong), ("lr", ctypes.c_float)]
+                ("seed", ctypes.c_ulonglong), ("lr", ctypes.c_float), ("attn_impl", ctypes.c_int)]
 
 
 class BatchStats(ctypes.Structure):
@@ -147,9 +147,13 @@ def mp_param_count(l, h, s, V):
     return _sym("mp_param_count")(l, h, s, V)
 
 
+ATTN = {"unfused": 0, "fused": 1}
+
+
 def make_cfg(l, h, a, s, V, dtype="bf16", p_drop_attn=0.0, p_drop_hidden=0.0, ln_eps=1e-5, recompute=False,
-             seed=1234, lr=1e-4):
-    return ModelCfg(l, h, a, s, V, DTYPES[dtype], p_drop_attn, p_drop_hidden, ln_eps, int(recompute), seed, lr)
+             seed=1234, lr=1e-4, attn="unfused"):
+    return ModelCfg(l, h, a, s, V, DTYPES[dtype], p_drop_attn, p_drop_hidden, ln_eps, int(recompute), seed, lr,
+                    ATTN[attn])
 
 
 def mp_validate(cfg, t, p, v, d, B=0, b=1, sched="interleaved"):

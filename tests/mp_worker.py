@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--dtype", default="bf16")
     ap.add_argument("--h", type=int, default=64)
     ap.add_argument("--l", type=int, default=4)
+    ap.add_argument("--attn", default="unfused")
     ap.add_argument("--out", default="")
     # arguments come through MP_WORKER_ARGS: torchrun's own parser would
     # otherwise claim any option that prefixes one of its flags (--m, --t ...)
@@ -47,10 +48,10 @@ def main():
     dist.init_process_group("gloo", init_method="env://")
     nid = [mp.mp_nccl_get_id() if rank == 0 else None]
     dist.broadcast_object_list(nid, src=0)
-    shape = gen.ModelCfg(l=a.l, h=a.h, a=4, s=32, V=512)
+    shape = gen.ModelCfg(l=a.l, h=a.h, a=4, s=32 if a.attn == "unfused" else 64, V=512)
     W = gen.model_weights(shape, seed=42, dtype=a.dtype)
     tok = gen.tokens(a.m, shape.s, shape.V, seed=1234)
-    cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype)
+    cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype, attn=a.attn)
     ctx = mp.Context(a.t, a.p, a.v, 1, cfg, rank, world, local, nid[0])
     tp, pp = rank % a.t, (rank // a.t) % a.p
     tol = {"bf16": 2e-2, "fp32": 1e-4}[a.dtype]

@@ -14,8 +14,8 @@ from tests.gpu_util import TOL, dev, host, normwise
 pytestmark = pytest.mark.gpu
 
 
-def make_ctx(cfg_shape, dtype, t=1, p=1, v=1, l=None):
-    c = mp.make_cfg(l or cfg_shape.l, cfg_shape.h, cfg_shape.a, cfg_shape.s, cfg_shape.V, dtype=dtype)
+def make_ctx(cfg_shape, dtype, t=1, p=1, v=1, l=None, attn="unfused"):
+    c = mp.make_cfg(l or cfg_shape.l, cfg_shape.h, cfg_shape.a, cfg_shape.s, cfg_shape.V, dtype=dtype, attn=attn)
     return mp.Context(t, p, v, 1, c, 0, 1, 0, mp.mp_nccl_get_id())
 
 
@@ -34,9 +34,9 @@ LAYER_CASES = [
 ]
 
 
-@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("dtype,attn", [("fp32", "unfused"), ("bf16", "unfused"), ("bf16", "fused")])
 @pytest.mark.parametrize("name,shape,b", LAYER_CASES)
-def test_layer_fwd_bwd(dtype, name, shape, b):
+def test_layer_fwd_bwd(dtype, attn, name, shape, b):
     if shape.s % 8 and dtype == "bf16":
         pytest.skip("bf16 kernels need s % 8 == 0")
     if shape.s % 4 and dtype == "fp32":
@@ -44,7 +44,7 @@ def test_layer_fwd_bwd(dtype, name, shape, b):
     W = gen.layer_weights(shape.h, 4, seed=11, layer=0, dtype=dtype)
     X = gen.activations((shape.s, b, shape.h), 12, 1.0, dtype)
     dY = gen.activations((shape.s, b, shape.h), 13, 1.0, dtype)
-    ctx = make_ctx(shape, dtype)
+    ctx = make_ctx(shape, dtype, attn=attn)
     try:
         for k, arr in W.items():
             ctx.set_weights(k, 0, arr)
@@ -66,14 +66,14 @@ def test_layer_fwd_bwd(dtype, name, shape, b):
         ctx.close()
 
 
-@pytest.mark.parametrize("dtype", ["bf16"])
-def test_layer_paper_width_1_7b(dtype):
+@pytest.mark.parametrize("dtype,attn", [("bf16", "unfused"), ("bf16", "fused")])
+def test_layer_paper_width_1_7b(dtype, attn):
     """One layer at the 1.7B config's width (h=2304, a=24, hd=96, s=2048, b=1)."""
     shape = gen.ModelCfg(l=1, h=2304, a=24, s=2048, V=51200)
     W = gen.layer_weights(shape.h, 24, seed=21, layer=0, dtype=dtype)
     X = gen.activations((shape.s, 1, shape.h), 22, 1.0, dtype)
     dY = gen.activations((shape.s, 1, shape.h), 23, 1.0, dtype)
-    ctx = make_ctx(shape, dtype)
+    ctx = make_ctx(shape, dtype, attn=attn)
     try:
         for k, arr in W.items():
             ctx.set_weights(k, 0, arr)
@@ -98,12 +98,21 @@ def test_layer_paper_width_1_7b(dtype):
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("sched,v,m", [("gpipe", 1, 4), ("1f1b", 1, 4), ("interleaved", 2, 4), ("interleaved", 4, 2)])
 def test_run_batch_single_gpu(dtype, sched, v, m):
+    _run_batch_case(gen.TINY, dtype, sched, v, m, "unfused")
+
+
+@pytest.mark.parametrize("sched,v,m", [("1f1b", 1, 4), ("interleaved", 2, 4)])
+def test_run_batch_fused_attention(sched, v, m):
+    """Same batch with the fused tcgen05 attention core (hd = 32 model)."""
+    _run_batch_case(gen.ModelCfg(l=4, h=128, a=4, s=64, V=512), "bf16", sched, v, m, "fused")
+
+
+def _run_batch_case(shape, dtype, sched, v, m, attn):
     """Tiny GPT (BASELINE config 0 shapes), whole batch through mp_run_batch on
     one GPU (p = 1, t = 1): loss and every gradient vs the oracle."""
-    shape = gen.TINY
     W = gen.model_weights(shape, seed=42, dtype=dtype)
     tok = gen.tokens(m, shape.s, shape.V, seed=1234)
-    ctx = make_ctx(shape, dtype, v=v)
+    ctx = make_ctx(shape, dtype, v=v, attn=attn)
     try:
         load_model(ctx, W)
         loss, stats = ctx.run_batch(m, 1, m, sched, tok)

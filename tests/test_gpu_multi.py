@@ -51,3 +51,22 @@ def test_multi_gpu_parity(tmp_path, t, p, v, m, sched, dtype):
     assert len(reps) == n and all(x["ok"] for x in reps), msg
     # every rank reports the same loss (shared after the flush)
     assert len({round(x["loss"][0], 6) for x in reps}) == 1, msg
+
+
+@pytest.mark.parametrize("t,p,v,m,sched", [(2, 2, 2, 4, "interleaved"), (2, 1, 1, 4, "1f1b"), (1, 4, 2, 4, "interleaved")])
+def test_multi_gpu_parity_fused_attention(tmp_path, t, p, v, m, sched):
+    """The same parity with the fused tcgen05 attention core (h = 128, hd = 32, s = 64)."""
+    n = t * p
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = str(tmp_path / "rep")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={31000 + (hash((t, p, v, m, sched)) % 2000)}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype bf16 "
+                                          f"--h 128 --l {max(4, p * v)} --attn fused --out {out}")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
+    msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
+    assert r.returncode == 0, msg
+    assert len(reps) == n and all(x["ok"] for x in reps), msg
