@@ -30,6 +30,12 @@
 
 namespace mp {
 
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 namespace fa {
 constexpr int BQ = 128, BKV = 128;
 constexpr int THREADS = 192;
@@ -164,21 +170,24 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tc_fence_after();
       const bool diag = j == qt;
       const uint32_t sa = tmem + lane_off + sb * 128;
-      // pass 1: row max of the scaled, masked scores
+      // the whole S row (128 fp32) into registers with one wait; the TMEM tile is then free
+      uint32_t sv[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(sa + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(sv + 32 * c));
+      tmem_ld_wait();
+      tc_fence_before();
+      mbar_arrive(&s_empty[sb]);
       float mx = -FLT_MAX;
+      if (diag) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(sa + 32 * c, v);
-        tmem_ld_wait();
+        for (int e = 0; e < 128; ++e)
+          if (e <= r) mx = fmaxf(mx, __uint_as_float(sv[e]));
+      } else {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int col = 32 * c + e;
-          if (!diag || col <= r) mx = fmaxf(mx, __uint_as_float(v[e]));
-        }
+        for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
       }
       const float m_new = fmaxf(m, mx * g.scale_log2);
-      const float alpha = exp2f(m - m_new);
+      const float alpha = ex2f(m - m_new);
       // P(j-1) has been consumed and O(j-1) is complete: rescale O and reuse the P tile
       if (j > 0) {
         mbar_wait(o_ready, (j - 1) & 1);
@@ -195,23 +204,22 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           tmem_st_wait();
         }
       }
-      // pass 2: P = exp2(s * scale_log2 - m_new) -> bf16 into the swizzled P tile
+      // P = exp2(s * scale_log2 - m_new) -> bf16 into the swizzled P tile
       float rs = 0.f;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(sa + 32 * c, v);
-        tmem_ld_wait();
         uint32_t w[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const int col = 32 * c + e;
-          float p0 = (!diag || col <= r) ? exp2f(__uint_as_float(v[e]) * g.scale_log2 - m_new) : 0.f;
-          float p1 = (!diag || col + 1 <= r) ? exp2f(__uint_as_float(v[e + 1]) * g.scale_log2 - m_new) : 0.f;
+          float p0 = ex2f(fmaf(__uint_as_float(sv[col]), g.scale_log2, -m_new));
+          float p1 = ex2f(fmaf(__uint_as_float(sv[col + 1]), g.scale_log2, -m_new));
+          if (diag) {
+            if (col > r) p0 = 0.f;
+            if (col + 1 > r) p1 = 0.f;
+          }
+          rs += p0 + p1;
           __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
-          // the row sum uses the rounded values the P.V product consumes
-          const float2 f = __bfloat1622float2(pr);
-          rs += f.x + f.y;
           w[e / 2] = *reinterpret_cast<uint32_t*>(&pr);
         }
         // columns 32c..32c+31 = kv block (c/2), 16-byte chunks 4(c%2)..4(c%2)+3
@@ -223,7 +231,6 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
       }
       tc_fence_before();
-      mbar_arrive(&s_empty[sb]);
       l = l * alpha + rs;
       m = m_new;
       fence_proxy_async_smem();        // P written by the generic proxy, read by tcgen05.mma
@@ -391,12 +398,20 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int quarter = warp % 4;
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    float l2n = 0.f, ddn = 0.f;
+    {
+      const int q0 = kt * 128 + r;
+      if (q0 < g.s) { l2n = g.L2[(long long)z * g.s + q0]; ddn = g.D[(long long)z * g.s + q0]; }
+    }
     for (int it = 0; it < niter; ++it) {
       const int qi = kt + it;
       const int q = qi * 128 + r;
       const bool qok = q < g.s;
-      const float l2 = qok ? g.L2[(long long)z * g.s + q] : 0.f;
-      const float dd = qok ? g.D[(long long)z * g.s + q] : 0.f;
+      const float l2 = l2n, dd = ddn;
+      if (it + 1 < niter && q + 128 < g.s) {        // prefetch the next tile's row statistics
+        l2n = g.L2[(long long)z * g.s + q + 128];
+        ddn = g.D[(long long)z * g.s + q + 128];
+      }
       const bool diag = it == 0;
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
@@ -415,7 +430,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           for (int u = 0; u < 2; ++u) {
             const int col = 32 * c + e + u;
             const bool vis = qok && (!diag || col <= r);
-            p[u] = vis ? exp2f(__uint_as_float(sv[e + u]) * g.scale_log2 - l2) : 0.f;
+            p[u] = vis ? ex2f(fmaf(__uint_as_float(sv[e + u]), g.scale_log2, -l2)) : 0.f;
             ds[u] = p[u] * (__uint_as_float(dv[e + u]) - dd) * g.scale;
           }
           __nv_bfloat162 pp = __floats2bfloat162_rn(p[0], p[1]);
