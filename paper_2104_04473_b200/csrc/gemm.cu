@@ -33,7 +33,7 @@ namespace mp {
 
 constexpr int BM = 128;
 constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
-constexpr int EPI_WARPS = 4;
+constexpr int EPI_WARPS = 8;               // two warps per TMEM lane quarter
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
 template <int BN>
@@ -43,8 +43,8 @@ struct TcCfg {
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
-  // epilogue staging: per epilogue warp two 32-row x 128-byte boxes (TMA store)
-  static constexpr int STAGE_OUT_BYTES = EPI_WARPS * 2 * 4096;
+  // epilogue staging: per epilogue warp one 32-row x 128-byte box (TMA store)
+  static constexpr int STAGE_OUT_BYTES = EPI_WARPS * 4096;
   static constexpr int SMEM = STAGES * STAGE_BYTES + STAGE_OUT_BYTES + 1024 + 256;
 };
 
@@ -180,9 +180,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   } else {
     // -------------------------------------------------- epilogue
     const int quarter = warp % 4;            // TMEM lanes 32*quarter .. +31
+    const int half = (warp - 2) / 4;         // the two warps of a quarter take alternate column boxes
     int acc = 0; uint32_t acc_phase = 0;
-    int obuf = 0;                            // staging buffer (double buffered per warp)
-    uint8_t* stage_base = sOut + (warp - 2) * 2 * 4096;
+    uint8_t* stage_base = sOut + (warp - 2) * 4096;
     for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
       const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
       const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
@@ -197,13 +197,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // TMEM -> registers -> 128B-swizzled staging box (32 rows x 128 B) -> TMA
         // store (bf16 / fp32) or TMA reduce-add (fp32 gradient accumulation).
         const int cw = g.c_fp32 ? 32 : 64;     // 128-byte rows: 32 fp32 or 64 bf16 columns per box
-        for (int c0 = 0; c0 < BN; c0 += cw) {
+        for (int c0 = half * cw; c0 < BN; c0 += 2 * cw) {
           const int col0 = n_blk * BN + c0;
           if (col0 >= g.N) break;
-          // the staging buffer written two boxes ago must have been read by its TMA
-          if (lane == 0) bulk_wait_read<1>();
+          // this warp's previous box must have been read by its TMA store
+          if (lane == 0) bulk_wait_read<0>();
           __syncwarp();
-          uint8_t* buf = stage_base + obuf * 4096;
+          uint8_t* buf = stage_base;
           const uint32_t rowaddr = smem_u32(buf) + lane * 128;
           if (g.c_fp32) {
             uint32_t r[32];
@@ -255,12 +255,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             else tma_store_3d(&tmC, buf, col0, row0, z);
             bulk_commit();
           }
-          obuf ^= 1;
         }
       } else {
         const int row = row0 + lane;
         const bool row_ok = row < g.M;
-        for (int c0 = 0; c0 < BN; c0 += 32) {
+        for (int c0 = half * 32; c0 < BN; c0 += 64) {
           const int col0 = n_blk * BN + c0;
           if (col0 >= g.N) break;
           uint32_t r[32];
