@@ -59,7 +59,9 @@ typedef struct {
   int V;                 /* vocabulary size */
   mp_dtype dtype;        /* storage/compute precision of the path (fp32 math inside bf16 kernels) */
   float p_drop_attn;     /* attention-probability dropout (reading #7); 0 = off */
-  float p_drop_hidden;   /* hidden dropout after proj / FC2; 0 = off */
+  float p_drop_hidden;   /* hidden dropout after proj / FC2; 0 = off.  Masks are Philox-4x32-10
+                            keyed by `seed` and each element's global (sequence, position, feature /
+                            head, query, key) coordinates, regenerated in the backward (reading #6) */
   float ln_eps;          /* LayerNorm epsilon (reading #2: 1e-5) */
   int recompute;         /* activation recomputation; counted by mp_flops only in round 1 */
   unsigned long long seed;  /* dropout stream key */

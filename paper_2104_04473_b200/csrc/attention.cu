@@ -26,6 +26,7 @@
 #include "common.h"
 #include "ptx.cuh"
 #include "tma_host.h"
+#include "dropout.cuh"
 #include "../../include/mp_ops.h"
 
 namespace mp {
@@ -54,6 +55,7 @@ struct FaArgs {
   long long ldo;               // row stride of O (b * heads * hd)
   float* L2;                   // [z, s]
   float scale_log2;
+  Dropout dp;                  // attention-probability dropout (off when dp.thresh == 0)
 };
 
 __global__ void __launch_bounds__(fa::THREADS, 1)
@@ -204,10 +206,21 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           tmem_st_wait();
         }
       }
-      // P = exp2(s * scale_log2 - m_new) -> bf16 into the swizzled P tile
+      // P = exp2(s * scale_log2 - m_new) -> bf16 into the swizzled P tile (dropped
+      // entries zeroed and kept ones scaled; the row sum uses the undropped values)
       float rs = 0.f;
+      const bool drop = g.dp.on();
+      const int zb = z / g.dp.heads, zj = z % g.dp.heads;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+        uint32_t km = 0xffffffffu;
+        if (drop) {
+          km = 0;
+          const unsigned long long e0 = (unsigned long long)qrow * g.s + j * BKV + 32 * c;
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            km |= keep4(g.dp, e0 / 4 + q4, g.dp.head0 + zj, g.dp.seq0 + zb) << (4 * q4);
+        }
         uint32_t w[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
@@ -219,6 +232,10 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             if (col + 1 > r) p1 = 0.f;
           }
           rs += p0 + p1;
+          if (drop) {
+            p0 = (km >> e) & 1 ? p0 * g.dp.scale : 0.f;
+            p1 = (km >> (e + 1)) & 1 ? p1 * g.dp.scale : 0.f;
+          }
           __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
           w[e / 2] = *reinterpret_cast<uint32_t*>(&pr);
         }
@@ -291,6 +308,7 @@ struct FabArgs {
   __nv_bfloat16* dQKV; // [s, b, heads, 3, hd]
   long long ldq;       // b * heads * 3 * hd
   float scale_log2, scale;
+  Dropout dp;
 };
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -416,12 +434,22 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
       const uint32_t prow = smem_u32(sP) + r * 128, dsrow = smem_u32(sdS) + r * 128;
+      const bool drop = g.dp.on();
+      const int zb = z / g.dp.heads, zj = z % g.dp.heads;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t sv[32], dv[32];
         tmem_ld_32x32b_x32(tmem + lane_off + 32 * c, sv);
         tmem_ld_32x32b_x32(tmem + lane_off + 128 + 32 * c, dv);
         tmem_ld_wait();
+        uint32_t km = 0xffffffffu;
+        if (drop) {
+          km = 0;
+          const unsigned long long e0 = (unsigned long long)q * g.s + kt * 128 + 32 * c;
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            km |= keep4(g.dp, e0 / 4 + q4, g.dp.head0 + zj, g.dp.seq0 + zb) << (4 * q4);
+        }
         uint32_t wp[16], wd[16];
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
@@ -430,8 +458,12 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           for (int u = 0; u < 2; ++u) {
             const int col = 32 * c + e + u;
             const bool vis = qok && (!diag || col <= r);
-            p[u] = vis ? ex2f(fmaf(__uint_as_float(sv[e + u]), g.scale_log2, -l2)) : 0.f;
-            ds[u] = p[u] * (__uint_as_float(dv[e + u]) - dd) * g.scale;
+            const float pr = vis ? ex2f(fmaf(__uint_as_float(sv[e + u]), g.scale_log2, -l2)) : 0.f;
+            const bool keep = (km >> (e + u)) & 1;
+            // dV uses the dropped probabilities; dP = mask * d(P_dropped)
+            const float dpv = drop ? (keep ? __uint_as_float(dv[e + u]) * g.dp.scale : 0.f) : __uint_as_float(dv[e + u]);
+            ds[u] = pr * (dpv - dd) * g.scale;
+            p[u] = drop ? (keep ? pr * g.dp.scale : 0.f) : pr;
           }
           __nv_bfloat162 pp = __floats2bfloat162_rn(p[0], p[1]);
           __nv_bfloat162 pd = __floats2bfloat162_rn(ds[0], ds[1]);
@@ -543,7 +575,8 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ acc, __nv_bfloat16
 // dQKV = d/dQKV of the fused attention, given O (= ctx), dO (= dctx), L2 from the forward.
 // workspace: fp32 [b*heads*s*hd + b*heads*s] (dQ accumulator, D).
 mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const float* L2, void* dQKV, float* ws,
-                         int s, int b, int heads, int hd, cudaStream_t st) {
+                         int s, int b, int heads, int hd, cudaStream_t st, Dropout dp) {
+  if (dp.on() && s % 4) return set_err(MP_EUNSUPPORTED, "fused attention dropout needs s %% 4 == 0");
   if (hd % 32 || hd > 128 || hd < 32) return set_err(MP_EUNSUPPORTED, "flash attention needs hd in {32,64,96,128}");
   const long long ldq = (long long)b * heads * 3 * hd, ldo = (long long)b * heads * hd;
   const long long zn = (long long)b * heads;
@@ -568,6 +601,7 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   a.L2 = L2; a.D = D; a.dQacc = dqacc; a.dQKV = reinterpret_cast<__nv_bfloat16*>(dQKV); a.ldq = ldq;
   a.scale = 1.f / std::sqrt((float)hd);
   a.scale_log2 = 1.4426950408889634f * a.scale;
+  a.dp = dp;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
@@ -588,7 +622,9 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
 }
 
 // QKV: [s, b, heads, 3, hd] bf16; O: [s, b, heads, hd] bf16; L2: [b*heads, s] fp32.
-mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st) {
+mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st,
+                         Dropout dp) {
+  if (dp.on() && s % 4) return set_err(MP_EUNSUPPORTED, "fused attention dropout needs s %% 4 == 0");
   if (hd % 32 || hd > 128 || hd < 32) return set_err(MP_EUNSUPPORTED, "flash attention needs hd in {32,64,96,128}");
   if (s < 1 || b < 1 || heads < 1) return set_err(MP_EINVAL, "flash attention: bad shape");
   const long long ldq = (long long)b * heads * 3 * hd;
@@ -606,6 +642,8 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
   a.ldo = (long long)b * heads * hd;
   a.L2 = L2;
   a.scale_log2 = 1.4426950408889634f / std::sqrt((float)hd);
+  a.dp = dp;
+  if (!dp.on()) a.dp.heads = 1;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(flash_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
@@ -630,11 +668,12 @@ extern "C" long long mp_op_flash_attn_bwd_ws_floats(int s, int b, int heads, int
 extern "C" mp_status mp_op_flash_attn_bwd(const void* qkv, const void* ctx, const void* dctx, const float* lse2,
                                           void* dqkv, float* ws, int s, int b, int heads, int hd, void* stream) {
   MP_REQUIRE_DEVICE();
-  return mp::flash_attn_bwd(qkv, ctx, dctx, lse2, dqkv, ws, s, b, heads, hd, reinterpret_cast<cudaStream_t>(stream));
+  return mp::flash_attn_bwd(qkv, ctx, dctx, lse2, dqkv, ws, s, b, heads, hd, reinterpret_cast<cudaStream_t>(stream),
+                            mp::Dropout{});
 }
 
 extern "C" mp_status mp_op_flash_attn_fwd(const void* qkv, void* ctx, float* lse2, int s, int b, int heads, int hd,
                                           void* stream) {
   MP_REQUIRE_DEVICE();
-  return mp::flash_attn_fwd(qkv, ctx, lse2, s, b, heads, hd, reinterpret_cast<cudaStream_t>(stream));
+  return mp::flash_attn_fwd(qkv, ctx, lse2, s, b, heads, hd, reinterpret_cast<cudaStream_t>(stream), mp::Dropout{});
 }

@@ -5,6 +5,7 @@
 // warp per row), reduces with warp shuffles, and computes in fp32.
 #include "kernels.cuh"
 #include "common.h"
+#include "dropout.cuh"
 
 #include <algorithm>
 #include <cfloat>
@@ -73,6 +74,14 @@ __device__ __forceinline__ float block_max(float a, float* red) {
   return r;
 }
 
+// keep bits of the V consecutive elements e0 .. e0+V-1 (e0 a multiple of V)
+template <int V>
+__device__ __forceinline__ uint32_t keep_bits(const Dropout& d, unsigned long long e0, uint32_t lane_hi, uint32_t n) {
+  uint32_t m = keep4(d, e0 / 4, lane_hi, n);
+  if (V == 8) m |= keep4(d, e0 / 4 + 1, lane_hi, n) << 4;
+  return m;
+}
+
 static int row_threads(int nvec) {
   int t = ((nvec + 3) / 4 + 31) / 32 * 32;   // <= 4 vectors per thread
   return std::max(32, std::min(256, t));
@@ -94,7 +103,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, c
                                                      const T* __restrict__ res, T* __restrict__ x1,
                                                      const T* __restrict__ g, const T* __restrict__ b,
                                                      T* __restrict__ out, float* __restrict__ mean,
-                                                     float* __restrict__ rstd, int h, float eps) {
+                                                     float* __restrict__ rstd, int h, float eps, Dropout dp) {
   constexpr int V = VW<T>::N;
   __shared__ float2 red[32];
   const long long row = blockIdx.x;
@@ -110,8 +119,15 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, c
         float bb[V], rr[V];
         ld_vec(bias + vi * V, bb);
         ld_vec(res + row * h + vi * V, rr);
+        if (dp.on()) {   // x1 = r + dropout(y + bias), mask keyed by (sequence, position, feature)
+          const int pos = (int)(row / dp.b), seq = dp.seq0 + (int)(row % dp.b);
+          const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * h + vi * V, 0, seq);
 #pragma unroll
-        for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
+          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + ((km >> e) & 1 ? (v[k][e] + bb[e]) * dp.scale : 0.f);
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
+        }
         st_vec(x1 + row * h + vi * V, v[k]);
         // LayerNorm consumes the stored (rounded) residual stream value
         ld_vec(x1 + row * h + vi * V, v[k]);
@@ -159,30 +175,39 @@ mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, f
                         cudaStream_t st) {
   MP_TRY(check_row_dims<T>(R, h));
   ln_fwd_kernel<T, 0><<<R, row_threads(h / VW<T>::N), 0, st>>>(x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, h,
-                                                                eps);
+                                                                eps, Dropout{});
   LAUNCH_CHECK();
 }
 
 template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
-                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st) {
+                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp) {
   MP_TRY(check_row_dims<T>(R, h));
-  ln_fwd_kernel<T, 1><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps);
+  ln_fwd_kernel<T, 1><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp);
   LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------ bias + residual add
 template <class T>
 __global__ void bias_add_residual_kernel(const T* __restrict__ yv, const T* __restrict__ bias,
-                                         const T* __restrict__ r, T* __restrict__ out, long long nvec, int hv) {
+                                         const T* __restrict__ r, T* __restrict__ out, long long nvec, int hv,
+                                         Dropout dp) {
   constexpr int V = VW<T>::N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
     float a[V], bb[V], rr[V];
     ld_vec(yv + i * V, a);
     ld_vec(bias + (i % hv) * V, bb);
     ld_vec(r + i * V, rr);
+    if (dp.on()) {
+      const long long row = i / hv;
+      const int pos = (int)(row / dp.b), seq = dp.seq0 + (int)(row % dp.b);
+      const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * hv * V + (i % hv) * V, 0, seq);
 #pragma unroll
-    for (int e = 0; e < V; ++e) a[e] = rr[e] + (a[e] + bb[e]);
+      for (int e = 0; e < V; ++e) a[e] = rr[e] + ((km >> e) & 1 ? (a[e] + bb[e]) * dp.scale : 0.f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < V; ++e) a[e] = rr[e] + (a[e] + bb[e]);
+    }
     st_vec(out + i * V, a);
   }
 }
@@ -193,11 +218,12 @@ static int ew_grid(long long nvec) {
 }
 
 template <class T>
-mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st) {
+mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st,
+                            Dropout dp) {
   constexpr int V = VW<T>::N;
   if (h % V) return set_err(MP_EINVAL, "bias_add_residual: h %% %d", V);
   long long nvec = R * h / V;
-  bias_add_residual_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V);
+  bias_add_residual_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V, dp);
   LAUNCH_CHECK();
 }
 
@@ -306,6 +332,41 @@ mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "colsum: N %% %d", V);
   colsum_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(X, out, R, N);
+  LAUNCH_CHECK();
+}
+
+// dZ = dropout mask * dY (written) and db[n] += sum_r dZ[r, n]   (hidden dropout backward)
+template <class T>
+__global__ void __launch_bounds__(CT_X * CT_Y) dropout_colsum_kernel(const T* __restrict__ dY, T* __restrict__ dZ,
+                                                                    float* __restrict__ out, int R, int N, Dropout dp) {
+  constexpr int V = VW<T>::N;
+  __shared__ float red[CT_Y * CT_X * V];
+  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
+  const int nv = N / V, vi = blockIdx.x * CT_X + tx;
+  const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
+  float acc[V] = {};
+  if (vi < nv) {
+    for (int r = r0 + ty; r < r1; r += CT_Y) {
+      float v[V];
+      ld_vec(dY + (long long)r * N + vi * V, v);
+      const int pos = r / dp.b, seq = dp.seq0 + r % dp.b;
+      const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * N + vi * V, 0, seq);
+#pragma unroll
+      for (int e = 0; e < V; ++e) v[e] = (km >> e) & 1 ? v[e] * dp.scale : 0.f;
+      st_vec(dZ + (long long)r * N + vi * V, v);
+      ld_vec(dZ + (long long)r * N + vi * V, v);   // the bias gradient sums the stored values
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] += v[e];
+    }
+  }
+  ct_reduce_add<V>(acc, red, out, vi, nv);
+}
+
+template <class T>
+mp_status dropout_colsum(const T* dY, T* dZ, float* out, int R, int N, Dropout dp, cudaStream_t st) {
+  constexpr int V = VW<T>::N;
+  if (N % V) return set_err(MP_EINVAL, "dropout_colsum: N %% %d", V);
+  dropout_colsum_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(dY, dZ, out, R, N, dp);
   LAUNCH_CHECK();
 }
 
@@ -501,12 +562,12 @@ __global__ void __launch_bounds__(SM_THREADS) softmax_fwd_kernel(T* __restrict__
 
 template <class T, int VPT>
 __global__ void __launch_bounds__(SM_THREADS) softmax_bwd_kernel(T* __restrict__ dP, const T* __restrict__ P, int s,
-                                                                 float scale) {
+                                                                 float scale, Dropout dp) {
   constexpr int V = VW<T>::N;
   __shared__ float red[4];
   const long long rg = blockIdx.x;
   const int i = (int)(rg % s);
-  T* dp = dP + rg * s;
+  T* dpr = dP + rg * s;
   const T* pp = P + rg * s;
   const int nv_read = i / V + 1;
   const int nv_write = causal_kend(i, s) / V;
@@ -516,8 +577,14 @@ __global__ void __launch_bounds__(SM_THREADS) softmax_bwd_kernel(T* __restrict__
   for (int k = 0; k < VPT; ++k) {
     const int vi = threadIdx.x + SM_THREADS * k;
     if (vi < nv_read) {
-      ld_vec(dp + vi * V, d[k]);
+      ld_vec(dpr + vi * V, d[k]);
       ld_vec(pp + vi * V, pv[k]);
+      if (dp.on()) {   // dP = dropout mask * d(P_dropped)
+        const int zz = (int)(rg / s), bb = zz / dp.heads, jj = zz % dp.heads;
+        const uint32_t km = keep_bits<V>(dp, (unsigned long long)i * s + vi * V, dp.head0 + jj, dp.seq0 + bb);
+#pragma unroll
+        for (int e = 0; e < V; ++e) d[k][e] = (km >> e) & 1 ? d[k][e] * dp.scale : 0.f;
+      }
 #pragma unroll
       for (int e = 0; e < V; ++e) {
         if (vi * V + e > i) { d[k][e] = 0.f; pv[k][e] = 0.f; }
@@ -533,7 +600,7 @@ __global__ void __launch_bounds__(SM_THREADS) softmax_bwd_kernel(T* __restrict__
       float o[V];
 #pragma unroll
       for (int e = 0; e < V; ++e) o[e] = vi < nv_read ? pv[k][e] * (d[k][e] - dot) * scale : 0.f;
-      st_vec(dp + vi * V, o);
+      st_vec(dpr + vi * V, o);
     }
   }
 }
@@ -563,16 +630,44 @@ mp_status softmax_causal_fwd(T* S, long long z, int s, float scale, cudaStream_t
 }
 
 template <class T>
-mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale, cudaStream_t st) {
+mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale, cudaStream_t st, Dropout dp) {
   constexpr int V = VW<T>::N;
   if (s % V) return set_err(MP_EINVAL, "softmax: s %% %d", V);
   const int vpt = softmax_vpt<T>(s);
   if (vpt < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
   const long long rows = z * s;
   if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "softmax: too many rows");
-  if (vpt == 1) softmax_bwd_kernel<T, 1><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale);
-  else if (vpt == 2) softmax_bwd_kernel<T, 2><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale);
-  else softmax_bwd_kernel<T, 4><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale);
+  if (vpt == 1) softmax_bwd_kernel<T, 1><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale, dp);
+  else if (vpt == 2) softmax_bwd_kernel<T, 2><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale, dp);
+  else softmax_bwd_kernel<T, 4><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale, dp);
+  LAUNCH_CHECK();
+}
+
+// Pd = dropout(P) over the written region j < kend(i) of a causal [z, s, s]
+// probability tensor (attention-probability dropout, unfused path).
+template <class T>
+__global__ void __launch_bounds__(SM_THREADS) attn_dropout_kernel(const T* __restrict__ P, T* __restrict__ Pd, int s,
+                                                                  Dropout dp) {
+  constexpr int V = VW<T>::N;
+  const long long rg = blockIdx.x;
+  const int i = (int)(rg % s);
+  const int zz = (int)(rg / s), bb = zz / dp.heads, jj = zz % dp.heads;
+  const int nv_write = causal_kend(i, s) / V;
+  for (int vi = threadIdx.x; vi < nv_write; vi += SM_THREADS) {
+    float v[V];
+    ld_vec(P + rg * s + vi * V, v);
+    const uint32_t km = keep_bits<V>(dp, (unsigned long long)i * s + vi * V, dp.head0 + jj, dp.seq0 + bb);
+#pragma unroll
+    for (int e = 0; e < V; ++e) v[e] = (km >> e) & 1 ? v[e] * dp.scale : 0.f;
+    st_vec(Pd + rg * s + vi * V, v);
+  }
+}
+
+template <class T>
+mp_status attn_dropout(const T* P, T* Pd, long long z, int s, Dropout dp, cudaStream_t st) {
+  const long long rows = z * s;
+  if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "attn_dropout: too many rows");
+  attn_dropout_kernel<T><<<(unsigned)rows, SM_THREADS, 0, st>>>(P, Pd, s, dp);
   LAUNCH_CHECK();
 }
 
@@ -753,15 +848,17 @@ mp_status cast_from_f32(const float* src, T* dst, long long n, cudaStream_t st) 
   template mp_status layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, float,             \
                                       cudaStream_t);                                                                \
   template mp_status bda_layernorm_fwd<T>(const T*, const T*, const T*, T*, const T*, const T*, T*, float*, float*,  \
-                                          int, int, float, cudaStream_t);                                           \
-  template mp_status bias_add_residual<T>(const T*, const T*, const T*, T*, long long, int, cudaStream_t);           \
+                                          int, int, float, cudaStream_t, Dropout);                                  \
+  template mp_status bias_add_residual<T>(const T*, const T*, const T*, T*, long long, int, cudaStream_t, Dropout);  \
+  template mp_status dropout_colsum<T>(const T*, T*, float*, int, int, Dropout, cudaStream_t);                      \
+  template mp_status attn_dropout<T>(const T*, T*, long long, int, Dropout, cudaStream_t);                          \
   template mp_status layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*,        \
                                       float*, float*, float*, int, int, cudaStream_t);                              \
   template mp_status bias_gelu_fwd<T>(const T*, const T*, T*, long long, int, cudaStream_t);                         \
   template mp_status bias_gelu_bwd<T>(const T*, const T*, const T*, T*, float*, int, int, cudaStream_t);             \
   template mp_status colsum_accum<T>(const T*, float*, int, int, cudaStream_t);                                     \
   template mp_status softmax_causal_fwd<T>(T*, long long, int, float, cudaStream_t);                                \
-  template mp_status softmax_causal_bwd<T>(T*, const T*, long long, int, float, cudaStream_t);                      \
+  template mp_status softmax_causal_bwd<T>(T*, const T*, long long, int, float, cudaStream_t, Dropout);             \
   template mp_status embed_fwd<T>(const int*, int, const T*, int, int, const T*, T*, int, int, int, cudaStream_t);  \
   template mp_status embed_bwd<T>(const int*, int, const T*, int, int, float*, float*, int, int, int, cudaStream_t); \
   template mp_status ce_loss_grad<T>(const float*, const float*, const float*, const int*, int, int, int, int,      \

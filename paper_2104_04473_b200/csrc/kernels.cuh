@@ -10,6 +10,7 @@
 #include <cstdint>
 
 #include "../../include/mp.h"
+#include "dropout.cuh"
 
 namespace mp {
 
@@ -23,10 +24,17 @@ mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, f
 // X1 = r + y + bias (written to x1), then A = LN(X1; g, b) (written to y).
 template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
-                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st);
-// out = r + y + bias
+                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp = Dropout{});
+// out = r + dropout(y + bias)
 template <class T>
-mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st);
+mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st,
+                            Dropout dp = Dropout{});
+// dZ = dropout mask * dY, db += colsum(dZ)   (hidden dropout backward)
+template <class T>
+mp_status dropout_colsum(const T* dY, T* dZ, float* db, int R, int N, Dropout dp, cudaStream_t st);
+// Pd = dropout(P) over the causal written region (unfused attention dropout)
+template <class T>
+mp_status attn_dropout(const T* P, T* Pd, long long z, int s, Dropout dp, cudaStream_t st);
 // dx = LN backward of dy (+ dres if non-null); dgamma/dbeta accumulated (fp32, +=).
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
@@ -45,7 +53,8 @@ template <class T>
 mp_status softmax_causal_fwd(T* S, long long z, int s, float scale, cudaStream_t st);
 // In-place dS = P * (dP - rowsum(dP * P)) * scale on dP.
 template <class T>
-mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale, cudaStream_t st);
+mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale, cudaStream_t st,
+                             Dropout dp = Dropout{});
 // X[i*b + beta] = (tok in [v0, v0+Vr) ? E[tok - v0] : 0) + (pos ? pos[i] : 0)
 template <class T>
 mp_status embed_fwd(const int* tok, int tok_ld, const T* E, int v0, int Vr, const T* pos, T* X, int s, int b, int h,

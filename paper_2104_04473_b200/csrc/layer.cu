@@ -26,9 +26,27 @@
 namespace mp {
 
 mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st);
-mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st);
+mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st,
+                         Dropout dp);
 mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const float* L2, void* dQKV, float* ws,
-                         int s, int b, int heads, int hd, cudaStream_t st);
+                         int s, int b, int heads, int hd, cudaStream_t st, Dropout dp);
+
+// Dropout streams of layer `layer` (reading #6): tensor 0 attention
+// probabilities, 1 hidden after the projection, 2 hidden after FC2.
+static Dropout make_dropout(const mp_ctx* c, int layer, int tensor, int seq0, int b) {
+  Dropout d;
+  const float p = tensor == 0 ? c->cfg.p_drop_attn : c->cfg.p_drop_hidden;
+  if (p <= 0.f) return d;
+  d.seed = c->cfg.seed;
+  d.stream = (uint32_t)(layer * 8 + tensor);
+  d.thresh = (uint32_t)std::floor((1.0 - (double)p) * 16777216.0);
+  d.scale = 1.f / (1.f - p);
+  d.seq0 = seq0;
+  d.b = b;
+  d.heads = c->cfg.a / c->t;
+  d.head0 = c->tp * d.heads;
+  return d;
+}
 
 static inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -126,7 +144,7 @@ static mp_status allreduce(mp_ctx* c, void* buf, size_t n, cudaStream_t st) {
 
 // ------------------------------------------------------------ attention
 template <class T>
-static mp_status attention_fwd(mp_ctx* c, const Dims& d, const void* QKV, void* P, void* ctx) {
+static mp_status attention_fwd(mp_ctx* c, const Dims& d, const void* QKV, void* P, void* ctx, const Dropout& dp) {
   const mp_dtype dt = c->cfg.dtype;
   const long long ldq = (long long)d.b * d.h3t;
   mp_gemm_desc g{};
@@ -138,10 +156,16 @@ static mp_status attention_fwd(mp_ctx* c, const Dims& d, const void* QKV, void* 
   g.c_fp32 = dt == MP_FP32;
   MP_TRY(gemm(dt, g, c->cs));
   MP_TRY(softmax_causal_fwd<T>(reinterpret_cast<T*>(P), d.z, d.s, 1.f / std::sqrt((float)d.hd), c->cs));
+  // attention-probability dropout: the P.V product reads dropout(P); P itself is stashed
+  const void* Pv = P;
+  if (dp.on()) {
+    MP_TRY(attn_dropout<T>(reinterpret_cast<const T*>(P), reinterpret_cast<T*>(c->ws_dsq), d.z, d.s, dp, c->cs));
+    Pv = c->ws_dsq;
+  }
   // ctx = P V  [s, b, heads, hd]
   g = mp_gemm_desc{};
   g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
-  g.A = P; g.lda = d.s; g.strideA = d.sq;
+  g.A = Pv; g.lda = d.s; g.strideA = d.sq;
   g.B = reinterpret_cast<const T*>(QKV) + 2 * d.hd; g.ldb = ldq; g.strideB = 3LL * d.hd; g.b_major = 1;
   g.C = ctx; g.ldc = (long long)d.b * d.ht; g.strideC = d.hd; g.alpha = 1.f; g.causal = 2;
   g.c_fp32 = dt == MP_FP32;
@@ -150,29 +174,34 @@ static mp_status attention_fwd(mp_ctx* c, const Dims& d, const void* QKV, void* 
 
 template <class T>
 static mp_status attention_bwd(mp_ctx* c, const Dims& d, const void* QKV, const void* P, const void* dctx,
-                               void* dP, void* dQKV) {
+                               void* dP, void* dQKV, const Dropout& dp) {
   const mp_dtype dt = c->cfg.dtype;
   const bool f32 = dt == MP_FP32;
   const long long ldq = (long long)d.b * d.h3t, ldc = (long long)d.b * d.ht;
   const T* Q = reinterpret_cast<const T*>(QKV);
   T* dQ = reinterpret_cast<T*>(dQKV);
   mp_gemm_desc g{};
+  // dV = dropout(P)^T dO  (dropout(P) regenerated into the dP workspace first)
+  const void* Pv = P;
+  if (dp.on()) {
+    MP_TRY(attn_dropout<T>(reinterpret_cast<const T*>(P), reinterpret_cast<T*>(dP), d.z, d.s, dp, c->cs));
+    Pv = dP;
+  }
+  g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
+  g.A = Pv; g.lda = d.s; g.strideA = d.sq; g.a_major = 1;
+  g.B = dctx; g.ldb = ldc; g.strideB = d.hd; g.b_major = 1;
+  g.C = dQ + 2 * d.hd; g.ldc = ldq; g.strideC = 3LL * d.hd; g.alpha = 1.f; g.causal = 3; g.c_fp32 = f32;
+  MP_TRY(gemm(dt, g, c->cs));
   // dP = dO V^T (causal tiles)
+  g = mp_gemm_desc{};
   g.M = d.s; g.N = d.s; g.K = d.hd; g.batch = (int)d.z;
   g.A = dctx; g.lda = ldc; g.strideA = d.hd;
   g.B = Q + 2 * d.hd; g.ldb = ldq; g.strideB = 3LL * d.hd;
   g.C = dP; g.ldc = d.s; g.strideC = d.sq; g.alpha = 1.f; g.causal = 1; g.c_fp32 = f32;
   MP_TRY(gemm(dt, g, c->cs));
-  // dV = P^T dO
-  g = mp_gemm_desc{};
-  g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
-  g.A = P; g.lda = d.s; g.strideA = d.sq; g.a_major = 1;
-  g.B = dctx; g.ldb = ldc; g.strideB = d.hd; g.b_major = 1;
-  g.C = dQ + 2 * d.hd; g.ldc = ldq; g.strideC = 3LL * d.hd; g.alpha = 1.f; g.causal = 3; g.c_fp32 = f32;
-  MP_TRY(gemm(dt, g, c->cs));
-  // dS = P (dP - rowsum(dP P)) / sqrt(hd), in place
+  // dS = P (dP - rowsum(dP P)) / sqrt(hd), in place (dP masked by the dropout first)
   MP_TRY(softmax_causal_bwd<T>(reinterpret_cast<T*>(dP), reinterpret_cast<const T*>(P), d.z, d.s,
-                               1.f / std::sqrt((float)d.hd), c->cs));
+                               1.f / std::sqrt((float)d.hd), c->cs, dp));
   // dQ = dS K
   g = mp_gemm_desc{};
   g.M = d.s; g.N = d.hd; g.K = d.s; g.batch = (int)d.z;
@@ -209,24 +238,27 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
   st.A = base + off[4]; st.QKV = base + off[5]; st.P = base + off[6]; st.ctx = base + off[7];
   st.X1 = base + off[8]; st.A2 = base + off[9]; st.Y1 = base + off[10]; st.H = base + off[11];
   st.b = b;
+  st.seq0 = c->cur_seq0;
+  const Dropout dpa = make_dropout(c, layer, 0, st.seq0, b), dp1 = make_dropout(c, layer, 1, st.seq0, b),
+                dp2 = make_dropout(c, layer, 2, st.seq0, b);
   const float eps = c->cfg.ln_eps;
   const T* X = reinterpret_cast<const T*>(x);
   MP_TRY(layernorm_fwd<T>(X, ptr<T>(c, lp[P_LN1G]), ptr<T>(c, lp[P_LN1B]), (T*)st.A, st.mu1, st.rs1, d.T, d.h, eps,
                           c->cs));
   MP_TRY(lin_fwd(c, st.A, ptr<T>(c, lp[P_WQKV]), ptr<T>(c, lp[P_BQKV]), st.QKV, d.T, d.h3t, d.h));
   if (use_fused(c))      // P holds the per-row base-2 log-sum-exp [z, s] instead of the scores
-    MP_TRY(flash_attn_fwd(st.QKV, st.ctx, (float*)st.P, d.s, d.b, d.heads, d.hd, c->cs));
+    MP_TRY(flash_attn_fwd(st.QKV, st.ctx, (float*)st.P, d.s, d.b, d.heads, d.hd, c->cs, dpa));
   else
-    MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx));
+    MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx, dpa));
   MP_TRY(lin_fwd(c, st.ctx, ptr<T>(c, lp[P_WO]), nullptr, c->ws_z, d.T, d.h, d.ht));
   MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
   MP_TRY(bda_layernorm_fwd<T>((const T*)c->ws_z, ptr<T>(c, lp[P_BO]), X, (T*)st.X1, ptr<T>(c, lp[P_LN2G]),
-                              ptr<T>(c, lp[P_LN2B]), (T*)st.A2, st.mu2, st.rs2, d.T, d.h, eps, c->cs));
+                              ptr<T>(c, lp[P_LN2B]), (T*)st.A2, st.mu2, st.rs2, d.T, d.h, eps, c->cs, dp1));
   MP_TRY(lin_fwd(c, st.A2, ptr<T>(c, lp[P_W1]), nullptr, st.Y1, d.T, d.h4t, d.h));
   MP_TRY(bias_gelu_fwd<T>((const T*)st.Y1, ptr<T>(c, lp[P_B1]), (T*)st.H, d.T, d.h4t, c->cs));
   MP_TRY(lin_fwd(c, st.H, ptr<T>(c, lp[P_W2]), nullptr, c->ws_z, d.T, d.h, d.h4t));
   MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
-  MP_TRY(bias_add_residual<T>((const T*)c->ws_z, ptr<T>(c, lp[P_B2]), (const T*)st.X1, (T*)y, d.T, d.h, c->cs));
+  MP_TRY(bias_add_residual<T>((const T*)c->ws_z, ptr<T>(c, lp[P_B2]), (const T*)st.X1, (T*)y, d.T, d.h, c->cs, dp2));
   return MP_OK;
 }
 
@@ -240,10 +272,18 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   T* dA2 = (T*)c->ws_dh1;
   T* dX1 = (T*)c->ws_dh2;
   cudaEvent_t ev_a = c->events.at(0), ev_b = c->events.at(1);
-  // MLP: dZ2 = dY (dropout p = 0); db2; dH = dY W2; dW2 += H^T dY
-  MP_TRY(colsum_accum<T>(dY, gptr(c, lp[P_B2]), d.T, d.h, c->cs));
-  MP_TRY(lin_dgrad(c, dY, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
-  MP_TRY(lin_wgrad(c, dY, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
+  const Dropout dpa = make_dropout(c, layer, 0, st.seq0, st.b), dp1 = make_dropout(c, layer, 1, st.seq0, st.b),
+                dp2 = make_dropout(c, layer, 2, st.seq0, st.b);
+  // MLP: dZ2 = dropout mask * dY; db2; dH = dZ2 W2; dW2 += H^T dZ2
+  const T* dZ2 = dY;
+  if (dp2.on()) {
+    MP_TRY(dropout_colsum<T>(dY, (T*)c->ws_z, gptr(c, lp[P_B2]), d.T, d.h, dp2, c->cs));
+    dZ2 = (const T*)c->ws_z;
+  } else {
+    MP_TRY(colsum_accum<T>(dY, gptr(c, lp[P_B2]), d.T, d.h, c->cs));
+  }
+  MP_TRY(lin_dgrad(c, dZ2, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
+  MP_TRY(lin_wgrad(c, dZ2, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
   MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]), d.T, d.h4t, c->cs));
   MP_TRY(lin_dgrad(c, dU, ptr<T>(c, lp[P_W1]), dA2, d.T, d.h4t, d.h));
   // f: all-reduce dA2 on the side stream while dW1 accumulates
@@ -257,15 +297,21 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   if (c->t > 1) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
   MP_TRY(layernorm_bwd<T>(dA2, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
                           gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs));
-  // attention block: dZ1 = dX1; dbo; dctx = dX1 Wo; dWo += ctx^T dX1
-  MP_TRY(colsum_accum<T>(dX1, gptr(c, lp[P_BO]), d.T, d.h, c->cs));
-  MP_TRY(lin_dgrad(c, dX1, ptr<T>(c, lp[P_WO]), c->ws_dctx, d.T, d.h, d.ht));
-  MP_TRY(lin_wgrad(c, dX1, st.ctx, gptr(c, lp[P_WO]), d.T, d.h, d.ht));
+  // attention block: dZ1 = dropout mask * dX1; dbo; dctx = dZ1 Wo; dWo += ctx^T dZ1
+  const T* dZ1 = dX1;
+  if (dp1.on()) {
+    MP_TRY(dropout_colsum<T>(dX1, (T*)c->ws_z, gptr(c, lp[P_BO]), d.T, d.h, dp1, c->cs));
+    dZ1 = (const T*)c->ws_z;
+  } else {
+    MP_TRY(colsum_accum<T>(dX1, gptr(c, lp[P_BO]), d.T, d.h, c->cs));
+  }
+  MP_TRY(lin_dgrad(c, dZ1, ptr<T>(c, lp[P_WO]), c->ws_dctx, d.T, d.h, d.ht));
+  MP_TRY(lin_wgrad(c, dZ1, st.ctx, gptr(c, lp[P_WO]), d.T, d.h, d.ht));
   if (use_fused(c))
     MP_TRY(flash_attn_bwd(st.QKV, st.ctx, c->ws_dctx, (const float*)st.P, c->ws_dqkv, c->ws_fa, d.s, d.b, d.heads,
-                          d.hd, c->cs));
+                          d.hd, c->cs, dpa));
   else
-    MP_TRY(attention_bwd<T>(c, d, st.QKV, st.P, c->ws_dctx, c->ws_dsq, c->ws_dqkv));
+    MP_TRY(attention_bwd<T>(c, d, st.QKV, st.P, c->ws_dctx, c->ws_dsq, c->ws_dqkv, dpa));
   MP_TRY(colsum_accum<T>((const T*)c->ws_dqkv, gptr(c, lp[P_BQKV]), d.T, d.h3t, c->cs));
   T* dA = (T*)c->ws_dh1;
   MP_TRY(lin_dgrad(c, c->ws_dqkv, ptr<T>(c, lp[P_WQKV]), dA, d.T, d.h3t, d.h));

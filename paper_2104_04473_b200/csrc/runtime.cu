@@ -162,8 +162,8 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
   MP_TRY(validate_cfg(cfg, t, p, v, d));
   if (t * p * d != world_size) return set_err(MP_EDIV, "t*p*d=%d != world size %d", t * p * d, world_size);
   if (world_rank < 0 || world_rank >= world_size) return set_err(MP_EINVAL, "bad rank");
-  if (cfg->p_drop_attn != 0.f || cfg->p_drop_hidden != 0.f)
-    return set_err(MP_EUNSUPPORTED, "dropout p > 0 is not built in this round (DESIGN.md)");
+  if (cfg->p_drop_attn < 0.f || cfg->p_drop_attn >= 1.f || cfg->p_drop_hidden < 0.f || cfg->p_drop_hidden >= 1.f)
+    return set_err(MP_EINVAL, "dropout rates must be in [0, 1)");
   if (cfg->dtype != MP_BF16 && cfg->dtype != MP_FP32) return set_err(MP_EINVAL, "bad dtype");
   if (p > 1) {
     // Six library streams (+ the caller's): fewer hardware queues create
@@ -352,6 +352,7 @@ mp_status mp_layer_fwd(mp_ctx* c, int layer, int b, const void* x, void* y, int*
   cudaStream_t saved = c->cs;
   c->cs = reinterpret_cast<cudaStream_t>(stream);   // NULL = legacy default stream (header contract)
   LayerStash st;
+  c->cur_seq0 = 0;
   const size_t bytes = (size_t)c->cfg.s * b * c->cfg.h * c->esz;
   mp_status s = alloc_async(c, &st.x, bytes, c->cs);
   if (s == MP_OK) {
@@ -429,6 +430,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
     if (dbg) fprintf(stderr, "[mp rank %d] enqueue %c mb=%d chunk=%d stage=%d\n", c->rank, tk.kind ? 'B' : 'F', tk.mb,
                      tk.chunk, sigma);
     const int* tok = dtok + (size_t)tk.mb * b * (s + 1);
+    c->cur_seq0 = tk.mb * b;        // global index of the microbatch's first sequence (dropout counters)
     if (tk.kind == 0) {
       // ------------------------------------------------------------ forward
       void* x = nullptr;

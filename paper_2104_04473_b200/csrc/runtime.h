@@ -39,6 +39,7 @@ struct LayerStash {
   float *mu1, *rs1, *mu2, *rs2;
   void *A, *QKV, *P, *ctx, *X1, *A2, *Y1, *H;
   int b = 1;
+  int seq0 = 0;        // global index of the microbatch's first sequence (dropout counters)
 };
 
 struct HeadStash {
@@ -85,6 +86,7 @@ struct mp_ctx {
   float* d_loss = nullptr;
   // events for task timing
   std::vector<cudaEvent_t> events;
+  int cur_seq0 = 0;                // set by the batch runtime before each microbatch task
   // pipeline channels (p > 1)
   mp::P2PRing p2p;
 };

@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--h", type=int, default=64)
     ap.add_argument("--l", type=int, default=4)
     ap.add_argument("--attn", default="unfused")
+    ap.add_argument("--pdrop", type=float, default=0.0)
     ap.add_argument("--out", default="")
     # arguments come through MP_WORKER_ARGS: torchrun's own parser would
     # otherwise claim any option that prefixes one of its flags (--m, --t ...)
@@ -51,7 +52,8 @@ def main():
     shape = gen.ModelCfg(l=a.l, h=a.h, a=4, s=32 if a.attn == "unfused" else 64, V=512)
     W = gen.model_weights(shape, seed=42, dtype=a.dtype)
     tok = gen.tokens(a.m, shape.s, shape.V, seed=1234)
-    cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype, attn=a.attn)
+    cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype, attn=a.attn,
+                      p_drop_attn=a.pdrop, p_drop_hidden=a.pdrop, seed=4321)
     ctx = mp.Context(a.t, a.p, a.v, 1, cfg, rank, world, local, nid[0])
     tp, pp = rank % a.t, (rank // a.t) % a.p
     tol = {"bf16": 2e-2, "fp32": 1e-4}[a.dtype]
@@ -63,7 +65,12 @@ def main():
         for name in ("emb", "pos", "lnf_g", "lnf_b"):
             ctx.set_weights(name, 0, W[name])
         loss, stats = ctx.run_batch(a.m, 1, a.m, a.sched, tok)
-        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m)
+        masks = None
+        if a.pdrop > 0:
+            from oracle import philox as PH
+            masks = [[PH.layer_masks(4321, k, [i], shape.s, shape.h, shape.a, a.pdrop, a.pdrop)
+                      for k in range(shape.l)] for i in range(a.m)]
+        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m, masks=masks)
         report["loss"] = [loss, lr]
         report["stats"] = stats
         ok = abs(loss - lr) / abs(lr) < tol

@@ -149,3 +149,65 @@ def test_run_batch_adam_step():
             assert np.max(np.abs(got - w1)) < 1e-5 + 1e-3 * 1e-2
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("dtype,attn", [("fp32", "unfused"), ("bf16", "unfused"), ("bf16", "fused")])
+def test_layer_dropout(dtype, attn):
+    """Attention-probability and hidden dropout (Philox masks keyed by global
+    coordinates, reading #6) against the oracle with the same masks."""
+    from oracle import philox as PH
+    shape, b, pa, ph = gen.ModelCfg(l=1, h=256, a=4, s=256, V=512), 2, 0.1, 0.15
+    W = gen.layer_weights(shape.h, 4, seed=61, layer=0, dtype=dtype)
+    X = gen.activations((shape.s, b, shape.h), 62, 1.0, dtype)
+    dY = gen.activations((shape.s, b, shape.h), 63, 1.0, dtype)
+    c = mp.make_cfg(1, shape.h, shape.a, shape.s, shape.V, dtype=dtype, attn=attn, p_drop_attn=pa, p_drop_hidden=ph,
+                    seed=777)
+    ctx = mp.Context(1, 1, 1, 1, c, 0, 1, 0, mp.mp_nccl_get_id())
+    try:
+        for k, arr in W.items():
+            ctx.set_weights(k, 0, arr)
+        ctx.zero_grads()
+        xd, yd = dev(X, dtype), dev(np.zeros_like(X), dtype)
+        slot = ctx.layer_fwd(0, b, xd.data_ptr(), yd.data_ptr())
+        dyd, dxd = dev(dY, dtype), dev(np.zeros_like(X), dtype)
+        ctx.layer_bwd(0, b, slot, dyd.data_ptr(), dxd.data_ptr())
+        torch.cuda.synchronize()
+        masks = PH.layer_masks(777, 0, list(range(b)), shape.s, shape.h, shape.a, pa, ph)
+        Yr, cache = L.layer_fwd(X, W, shape.a, masks)
+        dXr, gr = L.layer_bwd(dY, cache, W, shape.a, masks)
+        tol = TOL[dtype]
+        assert normwise(host(yd), Yr) < tol
+        assert normwise(host(dxd), dXr) < tol
+        for k in W:
+            g = ctx.get_grads(k, 0).reshape(gr[k].shape)
+            assert normwise(g, gr[k]) < tol, (k, normwise(g, gr[k]))
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("dtype,attn,h", [("fp32", "unfused", 64), ("bf16", "unfused", 64), ("bf16", "fused", 128)])
+def test_run_batch_dropout(dtype, attn, h):
+    from oracle import philox as PH
+    shape = gen.ModelCfg(l=4, h=h, a=4, s=32 if attn == "unfused" else 64, V=512)
+    m, pa, ph = 4, 0.1, 0.1
+    W = gen.model_weights(shape, seed=42, dtype=dtype)
+    tok = gen.tokens(m, shape.s, shape.V, seed=1234)
+    c = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=dtype, attn=attn, p_drop_attn=pa,
+                    p_drop_hidden=ph, seed=99)
+    ctx = mp.Context(1, 1, 2, 1, c, 0, 1, 0, mp.mp_nccl_get_id())
+    try:
+        load_model(ctx, W)
+        loss, _ = ctx.run_batch(m, 1, m, "interleaved", tok)
+        masks = [[PH.layer_masks(99, k, [i], shape.s, shape.h, shape.a, pa, ph) for k in range(shape.l)]
+                 for i in range(m)]
+        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, m, masks=masks)
+        tol = TOL[dtype]
+        assert abs(loss - lr) / abs(lr) < tol
+        for k in range(shape.l):
+            for name, ref in gr["layers"][k].items():
+                g = ctx.get_grads(name, k).reshape(ref.shape)
+                assert normwise(g, ref) < tol, (k, name, normwise(g, ref))
+        for name in ("emb", "pos"):
+            assert normwise(ctx.get_grads(name, 0).reshape(gr[name].shape), gr[name]) < tol, name
+    finally:
+        ctx.close()

@@ -70,3 +70,27 @@ def test_multi_gpu_parity_fused_attention(tmp_path, t, p, v, m, sched):
     msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
     assert r.returncode == 0, msg
     assert len(reps) == n and all(x["ok"] for x in reps), msg
+
+
+@pytest.mark.parametrize("t,p,v,m,sched,attn", [(2, 2, 2, 4, "interleaved", "unfused"), (2, 1, 1, 4, "1f1b", "fused")])
+def test_multi_gpu_parity_dropout(tmp_path, t, p, v, m, sched, attn):
+    """Dropout masks keyed by global coordinates are identical on every TP rank
+    and independent of the partition: results equal the oracle's."""
+    n = t * p
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = str(tmp_path / "rep")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={33000 + (hash((t, p, v, m, sched, attn)) % 2000)}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    h = 128 if attn == "fused" else 64
+    env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype fp32 "
+                                          f"--h {h} --attn {attn} --pdrop 0.1 --out {out}"
+               if attn == "unfused" else
+               f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype bf16 --h {h} --attn {attn} "
+               f"--pdrop 0.1 --out {out}")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
+    msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
+    assert r.returncode == 0, msg
+    assert len(reps) == n and all(x["ok"] for x in reps), msg
