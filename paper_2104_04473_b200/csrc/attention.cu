@@ -45,7 +45,11 @@ constexpr int Q_BYTES = 2 * BQ * 128;        // 2 hd-blocks of 64 (hd <= 128)
 constexpr int K_BYTES = 2 * BKV * 128;
 constexpr int V_BYTES = 2 * 2 * 64 * 128;    // [hd block][kv block] boxes of 64 x 64
 constexpr int P_BYTES = 2 * BQ * 128;        // 2 kv-blocks of 64
-constexpr int SMEM = Q_BYTES + 2 * (K_BYTES + V_BYTES) + P_BYTES + 1024 + 512;
+constexpr int SMEM = Q_BYTES + 2 * (K_BYTES + V_BYTES) + 2 * P_BYTES + 1024 + 512;   // P double buffered
+// Lazy rescaling: P is computed against a running reference max that is only
+// raised (and O, l rescaled) when the true row max exceeds it by more than
+// 2^8, so P <= 256 and most tiles never touch O (bf16 P / fp32 O have the range).
+constexpr float RESCALE_LOG2 = 8.f;
 constexpr int TMEM_COLS = 512;               // S[2] at 0 / 128, O at 256
 }  // namespace fa
 
@@ -58,6 +62,7 @@ struct FaArgs {
   Dropout dp;                  // attention-probability dropout (off when dp.thresh == 0)
 };
 
+template <bool DROP>
 __global__ void __launch_bounds__(fa::THREADS, 1)
 flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, FaArgs g) {
@@ -68,7 +73,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint8_t* sK = sQ + Q_BYTES;                  // [2 stages]
   uint8_t* sV = sK + 2 * K_BYTES;              // [2 stages]
   uint8_t* sP = sV + 2 * V_BYTES;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sP + 2 * P_BYTES);
   uint64_t* q_full = bar + 0;
   uint64_t* k_full = bar + 1;    // [2]
   uint64_t* v_full = bar + 3;    // [2]
@@ -76,7 +81,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint64_t* s_full = bar + 7;    // [2]
   uint64_t* s_empty = bar + 9;   // [2]
   uint64_t* p_full = bar + 11;
-  uint64_t* o_ready = bar + 12;
+  uint64_t* pv_done = bar + 12;  // [2]: PV of P buffer b complete (buffer reusable, O updated)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -92,7 +97,8 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 128);
     }
     mbar_init(p_full, 128);
-    mbar_init(o_ready, 1);
+    mbar_init(&pv_done[0], 1);
+    mbar_init(&pv_done[1], 1);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); }
@@ -131,7 +137,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_wait(p_full, jj & 1);
         mbar_wait(&v_full[st], (jj >> 1) & 1);
         tc_fence_after();
-        const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + st * V_BYTES);
+        const uint32_t pa = smem_u32(sP + (jj & 1) * P_BYTES), vb = smem_u32(sV + st * V_BYTES);
 #pragma unroll
         for (int k = 0; k < BKV / 16; ++k) {
           // P: K-major, 64-wide kv blocks 16 KB apart; V: MN-major, hd blocks 16 KB apart (LBO)
@@ -139,7 +145,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           const uint64_t bd = smem_desc_sw128(vb + (k / 4) * 8192 + (k % 4) * 2048, 16384, 1024);
           umma_f16(tmem + 256, ad, bd, idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
         }
-        umma_commit(o_ready);
+        umma_commit(&pv_done[jj & 1]);
         umma_commit(&kv_empty[st]);
       };
       for (int j = 0; j < nkv; ++j) {
@@ -164,8 +170,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     const int r = quarter * 32 + lane;                 // row within the tile
     const int qrow = qt * BQ + r;                      // query index
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    float m = -FLT_MAX, l = 0.f;
-    const uint32_t prow = smem_u32(sP) + r * 128;
+    float m = -FLT_MAX, l = 0.f;      // m: reference max (log2 units) P is computed against
     for (int j = 0; j < nkv; ++j) {
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
@@ -188,13 +193,17 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
         for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
       }
-      const float m_new = fmaxf(m, mx * g.scale_log2);
-      const float alpha = ex2f(m - m_new);
-      // P(j-1) has been consumed and O(j-1) is complete: rescale O and reuse the P tile
-      if (j > 0) {
-        mbar_wait(o_ready, (j - 1) & 1);
-        tc_fence_after();
-        if (__any_sync(0xffffffffu, alpha < 1.f)) {
+      const float mt = mx * g.scale_log2;
+      // raise the reference max only when this tile exceeds it by more than 2^RESCALE_LOG2
+      const bool need = __any_sync(0xffffffffu, mt > m + RESCALE_LOG2);
+      float alpha = 1.f;
+      if (need) {
+        const float m_new = fmaxf(m, mt);
+        alpha = ex2f(m - m_new);
+        m = m_new;
+        if (j > 0) {          // O holds P(0..j-1) V: wait for PV(j-1), then rescale it
+          mbar_wait(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          tc_fence_after();
           for (int c = 0; c < g.hd; c += 32) {
             uint32_t o[32];
             tmem_ld_32x32b_x32(tmem + lane_off + 256 + c, o);
@@ -206,10 +215,13 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           tmem_st_wait();
         }
       }
-      // P = exp2(s * scale_log2 - m_new) -> bf16 into the swizzled P tile (dropped
+      // the P buffer of tile j was last read by PV(j-2)
+      if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);
+      const uint32_t prow = smem_u32(sP + sb * P_BYTES) + r * 128;
+      // P = exp2(s * scale_log2 - m) -> bf16 into the swizzled P tile (dropped
       // entries zeroed and kept ones scaled; the row sum uses the undropped values)
       float rs = 0.f;
-      const bool drop = g.dp.on();
+      constexpr bool drop = DROP;
       const int zb = z / g.dp.heads, zj = z % g.dp.heads;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -225,8 +237,8 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const int col = 32 * c + e;
-          float p0 = ex2f(fmaf(__uint_as_float(sv[col]), g.scale_log2, -m_new));
-          float p1 = ex2f(fmaf(__uint_as_float(sv[col + 1]), g.scale_log2, -m_new));
+          float p0 = ex2f(fmaf(__uint_as_float(sv[col]), g.scale_log2, -m));
+          float p1 = ex2f(fmaf(__uint_as_float(sv[col + 1]), g.scale_log2, -m));
           if (diag) {
             if (col > r) p0 = 0.f;
             if (col + 1 > r) p1 = 0.f;
@@ -249,12 +261,11 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
       tc_fence_before();
       l = l * alpha + rs;
-      m = m_new;
       fence_proxy_async_smem();        // P written by the generic proxy, read by tcgen05.mma
       mbar_arrive(p_full);
     }
     // epilogue: O / l -> bf16 context row, L2 = m + log2(l)
-    mbar_wait(o_ready, (nkv - 1) & 1);
+    mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     tc_fence_after();
     const float inv = 1.f / l;
     const bool ok = qrow < g.s;
@@ -316,6 +327,7 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
                : "memory");
 }
 
+template <bool DROP>
 __global__ void __launch_bounds__(fa::THREADS, 1)
 flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, FabArgs g) {
@@ -434,7 +446,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
       const uint32_t prow = smem_u32(sP) + r * 128, dsrow = smem_u32(sdS) + r * 128;
-      const bool drop = g.dp.on();
+      constexpr bool drop = DROP;
       const int zb = z / g.dp.heads, zj = z % g.dp.heads;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
@@ -604,11 +616,14 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   a.dp = dp;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(flash_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(flash_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(flash_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
     if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  flash_bwd_kernel<<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, a);
+  if (dp.on()) flash_bwd_kernel<true><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, a);
+  else flash_bwd_kernel<false><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, a);
   count_launch();
   {
     const long long n = zn * s * hd / 2;
@@ -646,13 +661,16 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
   if (!dp.on()) a.dp.heads = 1;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(flash_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
+    cudaError_t e = cudaFuncSetAttribute(flash_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(flash_fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
     if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
   const long long grid = z * a.nq;
   if (grid > 0x7fffffffLL) return set_err(MP_EINVAL, "flash attention: grid too large");
-  flash_fwd_kernel<<<(unsigned)grid, fa::THREADS, fa::SMEM, st>>>(tq, tk, tv, a);
+  if (dp.on()) flash_fwd_kernel<true><<<(unsigned)grid, fa::THREADS, fa::SMEM, st>>>(tq, tk, tv, a);
+  else flash_fwd_kernel<false><<<(unsigned)grid, fa::THREADS, fa::SMEM, st>>>(tq, tk, tv, a);
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention launch: %s", cudaGetErrorString(e));
