@@ -30,6 +30,7 @@
 #include "../../include/mp_ops.h"
 
 namespace mp {
+extern long long* g_fa_trace;
 
 __device__ __forceinline__ float ex2f(float x) {
   float y;
@@ -60,7 +61,18 @@ struct FaArgs {
   float* L2;                   // [z, s]
   float scale_log2;
   Dropout dp;                  // attention-probability dropout (off when dp.thresh == 0)
+  long long* trace;            // debug: per-tile event timestamps of CTA 0 (null = off)
 };
+
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define FA_TRACE(ev, j)                                                         \
+  do {                                                                          \
+    if (g.trace && blockIdx.x == 0 && (j) < 64) g.trace[(ev) * 64 + (j)] = gtime(); \
+  } while (0)
 
 template <bool DROP>
 __global__ void __launch_bounds__(fa::THREADS, 1)
@@ -77,7 +89,8 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint64_t* q_full = bar + 0;
   uint64_t* k_full = bar + 1;    // [2]
   uint64_t* v_full = bar + 3;    // [2]
-  uint64_t* kv_empty = bar + 5;  // [2]
+  uint64_t* kv_empty = bar + 5;  // [2] K tile free (after its S product) -- V uses v_empty
+  uint64_t* v_empty = bar + 14;  // [2] V tile free (after its P.V product)
   uint64_t* s_full = bar + 7;    // [2]
   uint64_t* s_empty = bar + 9;   // [2]
   uint64_t* p_full = bar + 11;
@@ -93,7 +106,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&k_full[i], 1); mbar_init(&v_full[i], 1); mbar_init(&kv_empty[i], 1);
+      mbar_init(&k_full[i], 1); mbar_init(&v_full[i], 1); mbar_init(&kv_empty[i], 1); mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1); mbar_init(&s_empty[i], 128);
     }
     mbar_init(p_full, 128);
@@ -119,6 +132,9 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         mbar_arrive_expect_tx(&k_full[st], g.nhb * BKV * 128);
         for (int hb = 0; hb < g.nhb; ++hb)
           tma_load_3d(sK + st * K_BYTES + hb * BKV * 128, &tmK, &k_full[st], 64 * hb, j * BKV, z);
+        FA_TRACE(0, j);
+        if (j >= 2) mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        FA_TRACE(1, j);
         mbar_arrive_expect_tx(&v_full[st], g.nhb * 2 * 64 * 128);
         for (int hb = 0; hb < g.nhb; ++hb)
           for (int kb = 0; kb < 2; ++kb)
@@ -146,7 +162,8 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           umma_f16(tmem + 256, ad, bd, idesc_o, (jj > 0 || k > 0) ? 1u : 0u);
         }
         umma_commit(&pv_done[jj & 1]);
-        umma_commit(&kv_empty[st]);
+        umma_commit(&v_empty[st]);
+        FA_TRACE(3, jj);
       };
       for (int j = 0; j < nkv; ++j) {
         const int st = j & 1, sb = j & 1;
@@ -160,6 +177,8 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           umma_f16(tmem + sb * 128, ad, bd, idesc_s, k > 0 ? 1u : 0u);
         }
         umma_commit(&s_full[sb]);
+        umma_commit(&kv_empty[st]);       // K(j) consumed: the producer may refill this stage's K
+        FA_TRACE(2, j);
         if (j > 0) issue_pv(j - 1);
       }
       issue_pv(nkv - 1);
@@ -184,6 +203,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tmem_ld_wait();
       tc_fence_before();
       mbar_arrive(&s_empty[sb]);
+      if (threadIdx.x == 64) FA_TRACE(4, j);
       float mx = -FLT_MAX;
       if (diag) {
 #pragma unroll
@@ -215,6 +235,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           tmem_st_wait();
         }
       }
+      if (threadIdx.x == 64) FA_TRACE(5, j);
       // the P buffer of tile j was last read by PV(j-2)
       if (j >= 2) mbar_wait(&pv_done[sb], ((j - 2) >> 1) & 1);
       const uint32_t prow = smem_u32(sP + sb * P_BYTES) + r * 128;
@@ -263,6 +284,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       l = l * alpha + rs;
       fence_proxy_async_smem();        // P written by the generic proxy, read by tcgen05.mma
       mbar_arrive(p_full);
+      if (threadIdx.x == 64) FA_TRACE(6, j);
     }
     // epilogue: O / l -> bf16 context row, L2 = m + log2(l)
     mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
@@ -320,6 +342,7 @@ struct FabArgs {
   long long ldq;       // b * heads * 3 * hd
   float scale_log2, scale;
   Dropout dp;
+  long long* trace;
 };
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -330,7 +353,8 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 template <bool DROP>
 __global__ void __launch_bounds__(fa::THREADS, 1)
 flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, FabArgs g) {
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                 const __grid_constant__ CUtensorMap tmdQ, FabArgs g) {
   using namespace fab;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -361,7 +385,9 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     mbar_init(ds_ready, 128); mbar_init(dq_full, 1); mbar_init(tmem_free, 128);
     fence_mbar_init();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); }
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
+  }
   if (warp == 1) tmem_alloc<fa::TMEM_COLS>(tmem_slot);
   tc_fence_before();
   __syncthreads();
@@ -383,6 +409,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           tma_load_3d(sQ + hb * 16384, &tmQ, qd_full, 64 * hb, qi * 128, z);
           tma_load_3d(sdO + hb * 16384, &tmdO, qd_full, 64 * hb, qi * 128, z);
         }
+        FA_TRACE(0, it);
       }
     }
   } else if (warp == 1) {
@@ -406,6 +433,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                    k > 0 ? 1u : 0u);
         }
         umma_commit(sdp_full);
+        FA_TRACE(1, it);
         mbar_wait(ds_ready, it & 1);
         tc_fence_after();
         for (int k = 0; k < 8; ++k) {        // reductions over the 128 query rows / 128 keys
@@ -422,6 +450,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
         umma_commit(dq_full);
         umma_commit(qd_empty);
+        FA_TRACE(2, it);
       }
     }
   } else {
@@ -445,6 +474,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const bool diag = it == 0;
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
+      if (threadIdx.x == 64) FA_TRACE(3, it);
       const uint32_t prow = smem_u32(sP) + r * 128, dsrow = smem_u32(sdS) + r * 128;
       constexpr bool drop = DROP;
       const int zb = z / g.dp.heads, zj = z % g.dp.heads;
@@ -494,24 +524,51 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       fence_proxy_async_smem();
       tc_fence_before();
       mbar_arrive(ds_ready);
-      // dQ_i row -> fp32 reductions
+      if (threadIdx.x == 64) FA_TRACE(4, it);
+      // dQ_i tile -> fp32 TMA reduce-add into the dQ accumulator, staged through
+      // the P tile (free: the dV product that read it has completed)
       mbar_wait(dq_full, it & 1);
       tc_fence_after();
-      float* dqrow = g.dQacc + ((long long)z * g.s + q) * g.hd;
-      for (int c = 0; c < g.hd; c += 32) {
-        uint32_t v[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + 128 + c, v);
-        tmem_ld_wait();
-        if (qok) {
+      if (threadIdx.x == 64) FA_TRACE(5, it);
+      const int nchunk = g.hd / 32;
+      const uint32_t stg = smem_u32(sP);
+      for (int c0 = 0; c0 < nchunk; c0 += 2) {
+        uint32_t dqv[2][32];
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            red_add_v4(dqrow + c + e, __uint_as_float(v[e]), __uint_as_float(v[e + 1]), __uint_as_float(v[e + 2]),
-                       __uint_as_float(v[e + 3]));
+        for (int u = 0; u < 2; ++u)
+          if (c0 + u < nchunk) tmem_ld_32x32b_x32(tmem + lane_off + 128 + 32 * (c0 + u), dqv[u]);
+        tmem_ld_wait();
+        if (c0 + 2 >= nchunk) {
+          tc_fence_before();
+          mbar_arrive(tmem_free);      // the next S / dP products may now overwrite TMEM
+        }
+        if (c0 >= 2) {                 // boxes c0-2, c0-1 (same staging halves) must have been read
+          if (threadIdx.x == 64) bulk_wait_read<0>();
+          named_bar_sync(1, 128);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (c0 + u >= nchunk) break;
+          const uint32_t rowa = stg + u * 16384 + r * 128;
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            st_shared_v4(rowa + ((j ^ (r & 7)) << 4), dqv[u][4 * j], dqv[u][4 * j + 1], dqv[u][4 * j + 2],
+                         dqv[u][4 * j + 3]);
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (threadIdx.x == 64) {
+          for (int u = 0; u < 2 && c0 + u < nchunk; ++u)
+            tma_reduce_add_3d(&tmdQ, sP + u * 16384, 32 * (c0 + u), qi * 128, z);
+          bulk_commit();
         }
       }
-      tc_fence_before();
-      mbar_arrive(tmem_free);
+      // the P tile is rewritten by the next iteration: wait until the TMA has read it
+      if (threadIdx.x == 64) bulk_wait_read<0>();
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 64) FA_TRACE(6, it);
     }
+    if (threadIdx.x == 64) bulk_wait_all();
     // dK_j, dV_j rows (TMEM lane = key row) -> bf16 into the K / V slots of dQKV
     const int kvrow = kt * 128 + r;
     if (niter > 0) {
@@ -593,10 +650,11 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   const long long ldq = (long long)b * heads * 3 * hd, ldo = (long long)b * heads * hd;
   const long long zn = (long long)b * heads;
   const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(QKV);
-  CUtensorMap tq, tk, tv, tdo;
+  CUtensorMap tq, tk, tv, tdo, tdq;
   bool ok = make_map(&tq, q, hd, s, zn, ldq, 3LL * hd, 128) && make_map(&tk, q + hd, hd, s, zn, ldq, 3LL * hd, 128) &&
             make_map(&tv, q + 2 * hd, hd, s, zn, ldq, 3LL * hd, 128) &&
-            make_map(&tdo, dO, hd, s, zn, ldo, (long long)hd, 128);
+            make_map(&tdo, dO, hd, s, zn, ldo, (long long)hd, 128) &&
+            make_map(&tdq, ws, hd, s, zn, hd, (long long)s * hd, 128, 4);
   if (!ok) return set_err(MP_ECUDA, "flash attention bwd: tensor map encode failed");
   float* dqacc = ws;
   float* D = ws + zn * s * hd;
@@ -614,6 +672,16 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   a.scale = 1.f / std::sqrt((float)hd);
   a.scale_log2 = 1.4426950408889634f * a.scale;
   a.dp = dp;
+  a.trace = nullptr;
+  {
+    static long long* dtrace = nullptr;
+    if (getenv("MP_FA_TRACE")) {
+      if (!dtrace) cudaMalloc(&dtrace, 8 * 64 * sizeof(long long));
+      cudaMemsetAsync(dtrace, 0, 8 * 64 * sizeof(long long), st);
+      a.trace = dtrace;
+      g_fa_trace = dtrace;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(flash_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
@@ -622,8 +690,8 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
     if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  if (dp.on()) flash_bwd_kernel<true><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, a);
-  else flash_bwd_kernel<false><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, a);
+  if (dp.on()) flash_bwd_kernel<true><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
+  else flash_bwd_kernel<false><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
   count_launch();
   {
     const long long n = zn * s * hd / 2;
@@ -659,6 +727,17 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
   a.scale_log2 = 1.4426950408889634f / std::sqrt((float)hd);
   a.dp = dp;
   if (!dp.on()) a.dp.heads = 1;
+  a.trace = nullptr;
+  {
+    static long long* dtrace = nullptr;
+    if (getenv("MP_FA_TRACE")) {
+      if (!dtrace) cudaMalloc(&dtrace, 8 * 64 * sizeof(long long));
+      cudaMemsetAsync(dtrace, 0, 8 * 64 * sizeof(long long), st);
+      a.trace = dtrace;
+      extern long long* g_fa_trace;
+      g_fa_trace = dtrace;
+    }
+  }
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(flash_fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa::SMEM);
@@ -677,6 +756,8 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
   return MP_OK;
 }
 
+long long* g_fa_trace = nullptr;
+
 }  // namespace mp
 
 extern "C" long long mp_op_flash_attn_bwd_ws_floats(int s, int b, int heads, int hd) {
@@ -688,6 +769,10 @@ extern "C" mp_status mp_op_flash_attn_bwd(const void* qkv, const void* ctx, cons
   MP_REQUIRE_DEVICE();
   return mp::flash_attn_bwd(qkv, ctx, dctx, lse2, dqkv, ws, s, b, heads, hd, reinterpret_cast<cudaStream_t>(stream),
                             mp::Dropout{});
+}
+
+extern "C" void mp_debug_fa_trace(long long* host512) {
+  if (mp::g_fa_trace) cudaMemcpy(host512, mp::g_fa_trace, 8 * 64 * sizeof(long long), cudaMemcpyDeviceToHost);
 }
 
 extern "C" mp_status mp_op_flash_attn_fwd(const void* qkv, void* ctx, float* lse2, int s, int b, int heads, int hd,
