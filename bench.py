@@ -181,6 +181,79 @@ def run_reference(args, cfg, world, rank):
     print(json.dumps(out), flush=True)
 
 
+def replay_bubble(p, m, v, sched, tf, tb):
+    """Ideal-pipeline replay of the library's own static task orders (mp_get_schedule)
+    with this run's measured per-rank mean task durations and zero communication:
+    the bubble the schedule itself implies once stage imbalance (embedding on the
+    first stage, logit layer + loss on the last) is accounted for.  Returns the
+    per-rank idle share (span_r - busy_r) / busy_r, span measured from t = 0."""
+    from paper_2104_04473_b200 import mp
+    orders = [mp.mp_get_schedule(p, m, v, sched, r) for r in range(p)]
+    S = p * v
+    done, free, pos = {}, [0.0] * p, [0] * p
+    end = [0.0] * p
+    remaining = sum(len(o) for o in orders)
+    while remaining:
+        progressed = False
+        for r in range(p):
+            while pos[r] < len(orders[r]):
+                kind, i, c = orders[r][pos[r]]
+                sigma = c * p + r
+                if kind == "F":
+                    dep = None if sigma == 0 else ("F", i, sigma - 1)
+                else:
+                    dep = ("F", i, sigma) if sigma == S - 1 else ("B", i, sigma + 1)
+                if dep is not None and dep not in done:
+                    break
+                t0 = max(free[r], done[dep] if dep is not None else 0.0)
+                t1 = t0 + (tf[r] if kind == "F" else tb[r])
+                done[(kind, i, sigma)] = t1
+                free[r] = end[r] = t1
+                pos[r] += 1
+                remaining -= 1
+                progressed = True
+        if not progressed:
+            return None
+    busy = [m * v * (tf[r] + tb[r]) for r in range(p)]
+    return [(end[r] - busy[r]) / busy[r] for r in range(p)]
+
+
+def bubble_report(st, world, p, v, m, sched):
+    """Per-rank pipeline idle share of the last warm-up batch (max over ranks) next to
+    the closed form (p-1)/m or (p-1)/(v m), and the ideal-pipeline
+    estimate from this run's own per-task durations (equal stages assumed)."""
+    if not st:
+        return None
+    keys = ("bubble_measured", "pipeline_seconds", "busy_seconds", "t_fwd_task", "t_bwd_task", "iter_seconds")
+    vals = [st[k] for k in keys]
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        g = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(g, t)
+        per_rank = [x.tolist() for x in g]
+    else:
+        per_rank = [vals]
+    rep = {"formula": st["bubble_formula"], "schedule": sched, "p": p, "v": v, "m": m,
+           "measured_max_over_ranks": max(r[0] for r in per_rank),
+           "measured_per_rank": [round(r[0], 5) for r in per_rank],
+           "peak_inflight_rank0": st["peak_inflight"],
+           "t_fwd_task_s": [round(r[3], 6) for r in per_rank], "t_bwd_task_s": [round(r[4], 6) for r in per_rank],
+           "flush_and_optimizer_s": max(r[5] - r[1] for r in per_rank)}
+    if p > 1:
+        # pipeline stage r = the ranks with pp = r (TP ranks of a stage behave alike: use the max)
+        t = world // p
+        tf = [max(per_rank[r * t + k][3] for k in range(t)) for r in range(p)]
+        tb = [max(per_rank[r * t + k][4] for k in range(t)) for r in range(p)]
+        rp = replay_bubble(p, m, v, sched, tf, tb)
+        if rp:
+            rep["replay_per_stage"] = [round(x, 5) for x in rp]
+            rep["replay_note"] = ("same static orders, measured per-stage task durations, zero communication; "
+                                  "measured - replay = communication / launch stalls")
+    return rep
+
+
 def workload_config(args, cfg):
     t = args.t or max(1, args.gpus // args.p)
     sched = args.sched or ("interleaved" if args.v > 1 else "1f1b")
@@ -250,12 +323,14 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     l0 = mp.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    e0, e1 = ev[0], ev[-1]
     e0.record(stream)
-    for _ in range(args.steps):
+    for k in range(args.steps):
         ctx.run_batch_dev(B, b, m, sched, d_tok.data_ptr(), d_loss.data_ptr(), apply_optimizer=True)
-    e1.record(stream)
+        ev[k + 1].record(stream)
     torch.cuda.synchronize()
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     launches = mp.launch_count() - l0
     # GEMM roofline: the same iterations again with every GEMM launch bracketed by CUDA
     # events on its stream (kept out of the timed region above: ~2 events per launch
@@ -324,9 +399,9 @@ def main():
                      "how": "CUDA events around every GEMM launch on its stream, over --steps iterations "
                             "run right after the timed region"},
         "gpu_launches": int(launches),
+        "step_ms_rank0": [round(x, 3) for x in step_ms],
         "clocks": clk,
-        "bubble": ({k: wstats[k] for k in ("bubble_measured", "bubble_formula", "busy_seconds", "iter_seconds",
-                                           "peak_inflight")} if wstats else None),
+        "bubble": bubble_report(wstats, world, p, v, m, sched),
     }
     if e2e:
         out["e2e"] = e2e

@@ -77,10 +77,13 @@ typedef struct {
   double model_flops;           /* Eq. (2) F for this batch (72-variant without recompute) */
   double model_tflops_per_gpu;  /* F / (n * iter_seconds) / 1e12 */
   double busy_seconds;          /* sum of this rank's task durations (forward/backward chunk work) */
-  double bubble_measured;       /* (iter_seconds - busy)/busy on this rank */
+  double bubble_measured;       /* (pipeline_seconds - busy) / busy on this rank (P:104-105 t_pb / t_id) */
   double bubble_formula;        /* (p-1)/m or (p-1)/(v m) */
   int peak_inflight;            /* max stashed (microbatch, chunk) on this rank */
   int n_tasks;                  /* tasks executed on this rank (2 m v) */
+  double pipeline_seconds;      /* batch start -> end of this rank's last task (excludes the flush) */
+  double t_fwd_task;            /* mean forward-task (one chunk, one microbatch) duration on this rank */
+  double t_bwd_task;            /* mean backward-task duration on this rank */
 } mp_batch_stats;
 
 typedef struct mp_ctx mp_ctx;   /* opaque; one per process (= one GPU) */

@@ -582,19 +582,27 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   if (!stash.empty() || !local_act.empty() || !local_grad.empty())
     return set_err(MP_ESTATE, "pipeline finished with live activations (schedule bug)");
   if (stats) {
-    float ms = 0.f;
+    float ms = 0.f, pipe_ms = 0.f;
     cudaEventElapsedTime(&ms, ev_start, ev_end);
-    double busy = 0.0;
-    for (auto& pr : task_ev) {
+    if (!task_ev.empty()) cudaEventElapsedTime(&pipe_ms, ev_start, task_ev.back().second);
+    double busy = 0.0, tf = 0.0, tb = 0.0;
+    int nf = 0, nb = 0;
+    for (size_t i = 0; i < task_ev.size(); ++i) {
       float t = 0.f;
-      cudaEventElapsedTime(&t, pr.first, pr.second);
+      cudaEventElapsedTime(&t, task_ev[i].first, task_ev[i].second);
       busy += t;
+      if (tasks[i].kind == 0) { tf += t; ++nf; } else { tb += t; ++nb; }
     }
     stats->iter_seconds = ms * 1e-3;
     stats->busy_seconds = busy * 1e-3;
+    stats->pipeline_seconds = pipe_ms * 1e-3;
+    stats->t_fwd_task = nf ? tf * 1e-3 / nf : 0.0;
+    stats->t_bwd_task = nb ? tb * 1e-3 / nb : 0.0;
     stats->model_flops = mp_flops(B, s, c->cfg.l, h, c->cfg.V, c->cfg.recompute);
     stats->model_tflops_per_gpu = stats->model_flops / (c->world * stats->iter_seconds) / 1e12;
-    stats->bubble_measured = busy > 0 ? (ms - busy) / busy : 0.0;
+    // idle share of this rank between the batch start and its last task (the flush, the
+    // tied-embedding all-reduce and the optimizer step are not part of the bubble)
+    stats->bubble_measured = busy > 0 ? (pipe_ms - busy) / busy : 0.0;
     stats->bubble_formula = (double)(p - 1) / (sched == MP_INTERLEAVED ? (double)v * m : (double)m);
     stats->peak_inflight = peak;
     stats->n_tasks = (int)tasks.size();

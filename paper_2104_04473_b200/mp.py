@@ -48,7 +48,8 @@ class BatchStats(ctypes.Structure):
     _fields_ = [("iter_seconds", ctypes.c_double), ("model_flops", ctypes.c_double),
                 ("model_tflops_per_gpu", ctypes.c_double), ("busy_seconds", ctypes.c_double),
                 ("bubble_measured", ctypes.c_double), ("bubble_formula", ctypes.c_double),
-                ("peak_inflight", ctypes.c_int), ("n_tasks", ctypes.c_int)]
+                ("peak_inflight", ctypes.c_int), ("n_tasks", ctypes.c_int), ("pipeline_seconds", ctypes.c_double),
+                ("t_fwd_task", ctypes.c_double), ("t_bwd_task", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
