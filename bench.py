@@ -45,6 +45,8 @@ def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--tp-comm", dest="tp_comm", default="auto", choices=["auto", "nccl", "nvls"],
+                    help="transport of the layer all-reduces (auto: NVLS fused when available)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="1.7B", help="tiny | 1.7B | 7.5B | 18.4B | 39.1B")
@@ -291,7 +293,7 @@ def main():
     # ---- context (NCCL id from rank 0, broadcast by the launcher)
     from paper_2104_04473_b200 import launch
     nid = launch.share_bytes(mp.mp_nccl_get_id() if rank == 0 else None, rank, world)
-    c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5, attn=args.attn)
+    c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5, attn=args.attn, tp_comm=args.tp_comm)
     ctx = mp.Context(t, p, v, 1, c, rank, world, local, nid)
     # ---- random-init weights (only the owned shards are kept)
     dev_of, _ = mp.mp_get_stage_map(cfg.l, p, v)
@@ -384,7 +386,7 @@ def main():
         "metric": METRIC, "value": agg, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
-        "config": workload_config(args, cfg),
+        "config": dict(workload_config(args, cfg), tp_comm=ctx.tp_comm_mode()),
         "per_gpu_tflops": per_gpu,
         "pct_of_bf16_peak": {"measured_burst_1683": 100 * per_gpu / pk["bf16_burst"],
                              "measured_sustained": 100 * per_gpu / pk["bf16_sustained"],

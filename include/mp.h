@@ -49,6 +49,13 @@ typedef enum {
 
 typedef enum { MP_GPIPE = 0, MP_1F1B = 1, MP_INTERLEAVED = 2 } mp_schedule;
 typedef enum { MP_FP32 = 0, MP_BF16 = 1 } mp_dtype;
+/* Transport of the layer's g / f all-reduces when t > 1. */
+typedef enum {
+  MP_TP_COMM_AUTO = 0,   /* NVLS fused when the TP group has NVSwitch multicast, else NCCL */
+  MP_TP_COMM_NCCL = 1,   /* the paper's: ncclAllReduce of the partial product, then the elementwise kernel */
+  MP_TP_COMM_NVLS = 2    /* required: partials in an NCCL symmetric window, summed by the NVSwitch inside
+                            the consuming kernel's loads (multimem.ld_reduce); MP_EUNSUPPORTED if absent */
+} mp_tp_comm;
 
 /* GPT model shape (V = 51200, s = 2048 in the paper's models). */
 typedef struct {
@@ -69,6 +76,7 @@ typedef struct {
   int attn_impl;         /* 0: the paper's attention core -- strided-batched scores GEMM, fused
                             scale-mask-softmax, P.V GEMM; 1: fused tcgen05 flash kernel
                             (bf16, hd in {32,64,96,128}; otherwise falls back to 0) */
+  int tp_comm;           /* mp_tp_comm; the environment variable MP_TP_COMM=nccl overrides AUTO/NVLS */
 } mp_model_cfg;
 
 /* Per-batch statistics filled by mp_run_batch. */
@@ -189,6 +197,11 @@ mp_status mp_run_batch(mp_ctx* ctx, int B, int b, int m, mp_schedule sched, cons
  * stream every forward/backward task of mp_run_batch* is issued on, so that
  * callers can bracket batches with CUDA events on it. */
 void* mp_compute_stream(mp_ctx* ctx);
+
+/* Transport the layer's g / f all-reduces use on this rank: MP_TP_COMM_NCCL or
+ * MP_TP_COMM_NVLS (decided collectively at the first layer call with t > 1;
+ * MP_TP_COMM_AUTO before that; MP_TP_COMM_NCCL when t = 1, no collective). */
+int mp_tp_comm_mode(const mp_ctx* ctx);
 
 /* mp_run_batch with the inputs already resident in device memory: d_tokens
  * device int32 [B, s+1]; the mean loss is written (stream-ordered) to the

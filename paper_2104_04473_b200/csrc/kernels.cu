@@ -41,6 +41,29 @@ __device__ __forceinline__ void st_vec(__nv_bfloat16* p, const float* o) {
   *reinterpret_cast<uint4*>(p) = v;
 }
 
+// NVLS reduce-loads: `p` is a multicast address of a
+// TP-symmetric buffer; the NVSwitch returns the sum over the TP group's copies
+// (fp32 accumulation, one rounding to the storage type for bf16).
+__device__ __forceinline__ void ld_vec_red(const float* p, float* o) {
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(o[0]), "=f"(o[1]), "=f"(o[2]), "=f"(o[3]) : "l"(p) : "memory");
+}
+__device__ __forceinline__ void ld_vec_red(const __nv_bfloat16* p, float* o) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float2 f = __bfloat1622float2(h[i]);
+    o[2 * i] = f.x; o[2 * i + 1] = f.y;
+  }
+}
+template <bool RED, class T>
+__device__ __forceinline__ void ld_in(const T* p, float* o) {
+  if constexpr (RED) ld_vec_red(p, o); else ld_vec(p, o);
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
   for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -98,7 +121,7 @@ constexpr int LN_MAXV = 4;
 
 // ------------------------------------------------------------ LayerNorm fwd
 // mode 0: x = in; mode 1: x = r + yv + bias (bias-dropout-add with p = 0), x1 <- x.
-template <class T, int MODE>
+template <class T, int MODE, bool RED = false>
 __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, const T* __restrict__ bias,
                                                      const T* __restrict__ res, T* __restrict__ x1,
                                                      const T* __restrict__ g, const T* __restrict__ b,
@@ -114,7 +137,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, c
   for (int k = 0; k < LN_MAXV; ++k) {
     const int vi = threadIdx.x + k * blockDim.x;
     if (vi < nvec) {
-      ld_vec(in + row * h + vi * V, v[k]);
+      ld_in<RED>(in + row * h + vi * V, v[k]);
       if (MODE == 1) {
         float bb[V], rr[V];
         ld_vec(bias + vi * V, bb);
@@ -181,21 +204,25 @@ mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, f
 
 template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
-                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp) {
+                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp,
+                            bool red) {
   MP_TRY(check_row_dims<T>(R, h));
-  ln_fwd_kernel<T, 1><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp);
+  if (red)
+    ln_fwd_kernel<T, 1, true><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp);
+  else
+    ln_fwd_kernel<T, 1><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp);
   LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------ bias + residual add
-template <class T>
+template <class T, bool RED = false>
 __global__ void bias_add_residual_kernel(const T* __restrict__ yv, const T* __restrict__ bias,
                                          const T* __restrict__ r, T* __restrict__ out, long long nvec, int hv,
                                          Dropout dp) {
   constexpr int V = VW<T>::N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
     float a[V], bb[V], rr[V];
-    ld_vec(yv + i * V, a);
+    ld_in<RED>(yv + i * V, a);
     ld_vec(bias + (i % hv) * V, bb);
     ld_vec(r + i * V, rr);
     if (dp.on()) {
@@ -219,21 +246,26 @@ static int ew_grid(long long nvec) {
 
 template <class T>
 mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st,
-                            Dropout dp) {
+                            Dropout dp, bool red) {
   constexpr int V = VW<T>::N;
   if (h % V) return set_err(MP_EINVAL, "bias_add_residual: h %% %d", V);
   long long nvec = R * h / V;
-  bias_add_residual_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V, dp);
+  if (red)
+    bias_add_residual_kernel<T, true><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V, dp);
+  else
+    bias_add_residual_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V, dp);
   LAUNCH_CHECK();
 }
 
 // ------------------------------------------------------------ LayerNorm bwd
 // dx: one CTA per row (fp32 block sums of dxhat and dxhat*xhat).
-template <class T>
+// RED: dy is a multicast address (NVLS reduce-load of the TP partial sums); the
+// reduced rows are also stored to dy_copy for the gamma/beta kernel.
+template <class T, bool RED = false>
 __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                         const T* __restrict__ g, const float* __restrict__ mean,
                                                         const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                        T* __restrict__ dx, int h) {
+                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy) {
   constexpr int V = VW<T>::N;
   __shared__ float2 red[32];
   const long long row = blockIdx.x;
@@ -246,7 +278,8 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy
     const int vi = threadIdx.x + k * blockDim.x;
     if (vi < nvec) {
       float d[V], xv[V], gg[V];
-      ld_vec(dy + row * h + vi * V, d);
+      ld_in<RED>(dy + row * h + vi * V, d);
+      if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
       ld_vec(x + row * h + vi * V, xv);
       ld_vec(g + vi * V, gg);
 #pragma unroll
@@ -405,9 +438,14 @@ __global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel(const T* __restr
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
                         T* dx, float* dgamma, float* dbeta, float* /*scratch (unused)*/, int R, int h,
-                        cudaStream_t st) {
+                        cudaStream_t st, T* dy_copy) {
   MP_TRY(check_row_dims<T>(R, h));
-  ln_bwd_dx_kernel<T><<<R, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h);
+  if (dy_copy) {
+    ln_bwd_dx_kernel<T, true><<<R, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, dy_copy);
+    dy = dy_copy;
+  } else {
+    ln_bwd_dx_kernel<T><<<R, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, nullptr);
+  }
   count_launch();
   ln_bwd_gb_kernel<T><<<ct_grid(h / VW<T>::N, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dgamma, dbeta, R, h);
   LAUNCH_CHECK();
@@ -848,12 +886,13 @@ mp_status cast_from_f32(const float* src, T* dst, long long n, cudaStream_t st) 
   template mp_status layernorm_fwd<T>(const T*, const T*, const T*, T*, float*, float*, int, int, float,             \
                                       cudaStream_t);                                                                \
   template mp_status bda_layernorm_fwd<T>(const T*, const T*, const T*, T*, const T*, const T*, T*, float*, float*,  \
-                                          int, int, float, cudaStream_t, Dropout);                                  \
-  template mp_status bias_add_residual<T>(const T*, const T*, const T*, T*, long long, int, cudaStream_t, Dropout);  \
+                                          int, int, float, cudaStream_t, Dropout, bool);                            \
+  template mp_status bias_add_residual<T>(const T*, const T*, const T*, T*, long long, int, cudaStream_t, Dropout,   \
+                                          bool);                                                                    \
   template mp_status dropout_colsum<T>(const T*, T*, float*, int, int, Dropout, cudaStream_t);                      \
   template mp_status attn_dropout<T>(const T*, T*, long long, int, Dropout, cudaStream_t);                          \
   template mp_status layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*,        \
-                                      float*, float*, float*, int, int, cudaStream_t);                              \
+                                      float*, float*, float*, int, int, cudaStream_t, T*);                          \
   template mp_status bias_gelu_fwd<T>(const T*, const T*, T*, long long, int, cudaStream_t);                         \
   template mp_status bias_gelu_bwd<T>(const T*, const T*, const T*, T*, float*, int, int, cudaStream_t);             \
   template mp_status colsum_accum<T>(const T*, float*, int, int, cudaStream_t);                                     \

@@ -22,13 +22,16 @@ template <class T>
 mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int R, int h,
                         float eps, cudaStream_t st);
 // X1 = r + y + bias (written to x1), then A = LN(X1; g, b) (written to y).
+// red: yv is the multicast address of a TP-symmetric buffer and y is the NVLS
+// reduce-load of the t partial products (the g all-reduce fused into the load).
 template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
-                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp = Dropout{});
-// out = r + dropout(y + bias)
+                            float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp = Dropout{},
+                            bool red = false);
+// out = r + dropout(y + bias)   (red: as above)
 template <class T>
 mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long long R, int h, cudaStream_t st,
-                            Dropout dp = Dropout{});
+                            Dropout dp = Dropout{}, bool red = false);
 // dZ = dropout mask * dY, db += colsum(dZ)   (hidden dropout backward)
 template <class T>
 mp_status dropout_colsum(const T* dY, T* dZ, float* db, int R, int N, Dropout dp, cudaStream_t st);
@@ -36,9 +39,12 @@ mp_status dropout_colsum(const T* dY, T* dZ, float* db, int R, int N, Dropout dp
 template <class T>
 mp_status attn_dropout(const T* P, T* Pd, long long z, int s, Dropout dp, cudaStream_t st);
 // dx = LN backward of dy (+ dres if non-null); dgamma/dbeta accumulated (fp32, +=).
+// dy_copy non-null: dy is a multicast address, dy = NVLS reduce-load of the t
+// partials (the f all-reduce fused into the load), stored to dy_copy [R, h].
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
-                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st);
+                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st,
+                        T* dy_copy = nullptr);
 // H = gelu(Y + b)
 template <class T>
 mp_status bias_gelu_fwd(const T* yv, const T* b, T* out, long long R, int N, cudaStream_t st);

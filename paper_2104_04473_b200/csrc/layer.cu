@@ -17,6 +17,7 @@
 // gradients run on a side stream concurrently with the matching dW GEMM.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.h"
 #include "kernels.cuh"
@@ -117,6 +118,7 @@ mp_status alloc_async(mp_ctx* c, void** p, size_t bytes, cudaStream_t st) {
 }
 
 mp_status ensure_workspace(mp_ctx* c, int b) {
+  if (c->t > 1) MP_TRY(tp_sym_ensure(c, (size_t)c->cfg.s * b * c->cfg.h * c->esz));
   if (c->ws_b >= b) return MP_OK;
   MP_CUDA(cudaStreamSynchronize(c->cs));
   void** bufs[] = {&c->ws_z, &c->ws_dsq, &c->ws_d4h, &c->ws_dh1, &c->ws_dh2, &c->ws_dqkv, &c->ws_dctx};
@@ -139,6 +141,9 @@ mp_status ensure_workspace(mp_ctx* c, int b) {
 
 static mp_status allreduce(mp_ctx* c, void* buf, size_t n, cudaStream_t st) {
   if (c->t == 1) return MP_OK;
+  // timing experiments only (results are wrong): MP_DEBUG_SKIP_TP_AR=1 drops the layer all-reduces
+  static const bool skip = getenv("MP_DEBUG_SKIP_TP_AR") && atoi(getenv("MP_DEBUG_SKIP_TP_AR"));
+  if (skip) return MP_OK;
   return nccl_check(ncclAllReduce(buf, buf, n, c->nccl_dt, ncclSum, c->tp_comm, st), "tp all-reduce");
 }
 
@@ -250,15 +255,25 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
     MP_TRY(flash_attn_fwd(st.QKV, st.ctx, (float*)st.P, d.s, d.b, d.heads, d.hd, c->cs, dpa));
   else
     MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx, dpa));
-  MP_TRY(lin_fwd(c, st.ctx, ptr<T>(c, lp[P_WO]), nullptr, c->ws_z, d.T, d.h, d.ht));
-  MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
-  MP_TRY(bda_layernorm_fwd<T>((const T*)c->ws_z, ptr<T>(c, lp[P_BO]), X, (T*)st.X1, ptr<T>(c, lp[P_LN2G]),
-                              ptr<T>(c, lp[P_LN2B]), (T*)st.A2, st.mu2, st.rs2, d.T, d.h, eps, c->cs, dp1));
+  const bool nv = c->tps.on, nvr = nv && !tp_sym_debug_local();
+  void* zw; const void* zr;   // partial-product buffer: GEMM writes zw, the consumer reads zr
+  // g (a11): NCCL all-reduce in place, or NVLS barrier + reduce-load inside the consumer
+  auto g_op = [&]() -> mp_status { return nv ? tp_sym_barrier(c, c->cs) : allreduce(c, zw, (size_t)d.T * d.h, c->cs); };
+  auto z_next = [&]() {
+    if (nv) tp_sym_next(c, &zw, &zr); else { zw = c->ws_z; zr = c->ws_z; }
+    if (nv && !nvr) zr = zw;
+  };
+  z_next();
+  MP_TRY(lin_fwd(c, st.ctx, ptr<T>(c, lp[P_WO]), nullptr, zw, d.T, d.h, d.ht));
+  MP_TRY(g_op());
+  MP_TRY(bda_layernorm_fwd<T>((const T*)zr, ptr<T>(c, lp[P_BO]), X, (T*)st.X1, ptr<T>(c, lp[P_LN2G]),
+                              ptr<T>(c, lp[P_LN2B]), (T*)st.A2, st.mu2, st.rs2, d.T, d.h, eps, c->cs, dp1, nvr));
   MP_TRY(lin_fwd(c, st.A2, ptr<T>(c, lp[P_W1]), nullptr, st.Y1, d.T, d.h4t, d.h));
   MP_TRY(bias_gelu_fwd<T>((const T*)st.Y1, ptr<T>(c, lp[P_B1]), (T*)st.H, d.T, d.h4t, c->cs));
-  MP_TRY(lin_fwd(c, st.H, ptr<T>(c, lp[P_W2]), nullptr, c->ws_z, d.T, d.h, d.h4t));
-  MP_TRY(allreduce(c, c->ws_z, (size_t)d.T * d.h, c->cs));                       // g
-  MP_TRY(bias_add_residual<T>((const T*)c->ws_z, ptr<T>(c, lp[P_B2]), (const T*)st.X1, (T*)y, d.T, d.h, c->cs, dp2));
+  z_next();
+  MP_TRY(lin_fwd(c, st.H, ptr<T>(c, lp[P_W2]), nullptr, zw, d.T, d.h, d.h4t));
+  MP_TRY(g_op());
+  MP_TRY(bias_add_residual<T>((const T*)zr, ptr<T>(c, lp[P_B2]), (const T*)st.X1, (T*)y, d.T, d.h, c->cs, dp2, nvr));
   return MP_OK;
 }
 
@@ -285,18 +300,25 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   MP_TRY(lin_dgrad(c, dZ2, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
   MP_TRY(lin_wgrad(c, dZ2, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
   MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]), d.T, d.h4t, c->cs));
-  MP_TRY(lin_dgrad(c, dU, ptr<T>(c, lp[P_W1]), dA2, d.T, d.h4t, d.h));
-  // f: all-reduce dA2 on the side stream while dW1 accumulates
-  if (c->t > 1) {
+  // f (a17): NVLS -- dgrad writes its partial into the symmetric buffer, dW1 accumulates, one barrier,
+  // and the LayerNorm backward reduce-loads the sum; NCCL -- all-reduce dA2 on the side stream during dW1
+  const bool nv = c->tps.on, nvr = nv && !tp_sym_debug_local();
+  void* fw = dA2; const void* fr = dA2;
+  if (nv) tp_sym_next(c, &fw, &fr);
+  if (nv && !nvr) fr = fw;
+  MP_TRY(lin_dgrad(c, dU, ptr<T>(c, lp[P_W1]), fw, d.T, d.h4t, d.h));
+  if (c->t > 1 && !nv) {
     MP_CUDA(cudaEventRecord(ev_a, c->cs));
     MP_CUDA(cudaStreamWaitEvent(c->side, ev_a, 0));
     MP_TRY(allreduce(c, dA2, (size_t)d.T * d.h, c->side));
     MP_CUDA(cudaEventRecord(ev_b, c->side));
   }
   MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
-  if (c->t > 1) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
-  MP_TRY(layernorm_bwd<T>(dA2, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
-                          gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs));
+  if (c->t > 1 && !nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
+  if (nv) MP_TRY(tp_sym_barrier(c, c->cs));
+  MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
+                          gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs,
+                          nvr ? dA2 : nullptr));
   // attention block: dZ1 = dropout mask * dX1; dbo; dctx = dZ1 Wo; dWo += ctx^T dZ1
   const T* dZ1 = dX1;
   if (dp1.on()) {
@@ -314,17 +336,22 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
     MP_TRY(attention_bwd<T>(c, d, st.QKV, st.P, c->ws_dctx, c->ws_dsq, c->ws_dqkv, dpa));
   MP_TRY(colsum_accum<T>((const T*)c->ws_dqkv, gptr(c, lp[P_BQKV]), d.T, d.h3t, c->cs));
   T* dA = (T*)c->ws_dh1;
-  MP_TRY(lin_dgrad(c, c->ws_dqkv, ptr<T>(c, lp[P_WQKV]), dA, d.T, d.h3t, d.h));
-  if (c->t > 1) {
+  fw = dA; fr = dA;
+  if (nv) tp_sym_next(c, &fw, &fr);
+  if (nv && !nvr) fr = fw;
+  MP_TRY(lin_dgrad(c, c->ws_dqkv, ptr<T>(c, lp[P_WQKV]), fw, d.T, d.h3t, d.h));
+  if (c->t > 1 && !nv) {
     MP_CUDA(cudaEventRecord(ev_a, c->cs));
     MP_CUDA(cudaStreamWaitEvent(c->side, ev_a, 0));
     MP_TRY(allreduce(c, dA, (size_t)d.T * d.h, c->side));
     MP_CUDA(cudaEventRecord(ev_b, c->side));
   }
   MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
-  if (c->t > 1) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
-  MP_TRY(layernorm_bwd<T>(dA, (const T*)st.x, ptr<T>(c, lp[P_LN1G]), st.mu1, st.rs1, dX1, (T*)dx,
-                          gptr(c, lp[P_LN1G]), gptr(c, lp[P_LN1B]), c->ws_ln, d.T, d.h, c->cs));
+  if (c->t > 1 && !nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
+  if (nv) MP_TRY(tp_sym_barrier(c, c->cs));
+  MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.x, ptr<T>(c, lp[P_LN1G]), st.mu1, st.rs1, dX1, (T*)dx,
+                          gptr(c, lp[P_LN1G]), gptr(c, lp[P_LN1B]), c->ws_ln, d.T, d.h, c->cs,
+                          nvr ? dA : nullptr));
   return MP_OK;
 }
 

@@ -268,6 +268,7 @@ mp_status mp_finalize(mp_ctx* c) {
   for (auto& kv : c->slots) stash_release(c, kv.second, c->cs);
   cudaStreamSynchronize(c->cs);
   p2p_release(c);
+  tp_sym_free(c);
   ncclComm_t comms[] = {c->tp_comm, c->emb_comm, c->world_comm};
   for (auto cm : comms)
     if (cm) ncclCommDestroy(cm);
@@ -614,6 +615,13 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
 mp_status mp_run_batch(mp_ctx* c, int B, int b, int m, mp_schedule sched, const int* tokens, int apply_optimizer,
                        float* loss_out, mp_batch_stats* stats) {
   return run_batch_impl(c, B, b, m, sched, tokens, false, apply_optimizer, loss_out, nullptr, stats);
+}
+
+int mp_tp_comm_mode(const mp_ctx* c) {
+  if (!c) return MP_TP_COMM_AUTO;
+  if (c->t == 1) return MP_TP_COMM_NCCL;
+  if (!c->tps.tried) return MP_TP_COMM_AUTO;
+  return c->tps.on ? MP_TP_COMM_NVLS : MP_TP_COMM_NCCL;
 }
 
 void* mp_compute_stream(mp_ctx* c) { return c ? reinterpret_cast<void*>(c->cs) : nullptr; }

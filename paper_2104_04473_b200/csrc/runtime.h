@@ -12,6 +12,7 @@
 #include "../../include/mp.h"
 #include "p2p.h"
 #include "schedule.h"
+#include "tpcomm.h"
 
 namespace mp {
 
@@ -89,4 +90,6 @@ struct mp_ctx {
   int cur_seq0 = 0;                // set by the batch runtime before each microbatch task
   // pipeline channels (p > 1)
   mp::P2PRing p2p;
+  // TP-symmetric buffers of the fused g / f all-reduce (t > 1)
+  mp::TpSym tps;
 };

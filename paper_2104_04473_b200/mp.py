@@ -41,7 +41,8 @@ class ModelCfg(ctypes.Structure):
     _fields_ = [("l", ctypes.c_int), ("h", ctypes.c_int), ("a", ctypes.c_int), ("s", ctypes.c_int),
                 ("V", ctypes.c_int), ("dtype", ctypes.c_int), ("p_drop_attn", ctypes.c_float),
                 ("p_drop_hidden", ctypes.c_float), ("ln_eps", ctypes.c_float), ("recompute", ctypes.c_int),
-                ("seed", ctypes.c_ulonglong), ("lr", ctypes.c_float), ("attn_impl", ctypes.c_int)]
+                ("seed", ctypes.c_ulonglong), ("lr", ctypes.c_float), ("attn_impl", ctypes.c_int),
+                ("tp_comm", ctypes.c_int)]
 
 
 class BatchStats(ctypes.Structure):
@@ -88,6 +89,7 @@ SIGNATURES = {
     "mp_layer_bwd": (_I, [_P, _I, _I, _I, _P, _P, _P]),
     "mp_run_batch": (_I, [_P, _I, _I, _I, _I, _P, _I, ctypes.POINTER(_F), ctypes.POINTER(BatchStats)]),
     "mp_compute_stream": (_P, [_P]),
+    "mp_tp_comm_mode": (_I, [_P]),
     "mp_run_batch_dev": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, ctypes.POINTER(BatchStats)]),
     "mp_op_gemm": (_I, [_I, ctypes.POINTER(GemmDesc), _P]),
     "mp_gemm_flops": (_D, [ctypes.POINTER(GemmDesc)]),
@@ -151,10 +153,13 @@ def mp_param_count(l, h, s, V):
 ATTN = {"unfused": 0, "fused": 1}
 
 
+TP_COMM = {"auto": 0, "nccl": 1, "nvls": 2}
+
+
 def make_cfg(l, h, a, s, V, dtype="bf16", p_drop_attn=0.0, p_drop_hidden=0.0, ln_eps=1e-5, recompute=False,
-             seed=1234, lr=1e-4, attn="unfused"):
+             seed=1234, lr=1e-4, attn="unfused", tp_comm="auto"):
     return ModelCfg(l, h, a, s, V, DTYPES[dtype], p_drop_attn, p_drop_hidden, ln_eps, int(recompute), seed, lr,
-                    ATTN[attn])
+                    ATTN[attn], TP_COMM[tp_comm])
 
 
 def mp_validate(cfg, t, p, v, d, B=0, b=1, sched="interleaved"):
@@ -268,6 +273,10 @@ class Context:
 
     def stream(self):
         return _sym("mp_compute_stream")(self.ptr)
+
+    def tp_comm_mode(self):
+        """'nccl' / 'nvls' (the transport of the layer all-reduces), 'auto' before the first layer call."""
+        return {v: k for k, v in TP_COMM.items()}[_sym("mp_tp_comm_mode")(self.ptr)]
 
     def run_batch_dev(self, B, b, m, sched, d_tokens, d_loss, apply_optimizer=False, stats=False):
         """Device-resident variant: d_tokens / d_loss are device addresses."""

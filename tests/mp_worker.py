@@ -32,6 +32,7 @@ def main():
     ap.add_argument("--l", type=int, default=4)
     ap.add_argument("--attn", default="unfused")
     ap.add_argument("--pdrop", type=float, default=0.0)
+    ap.add_argument("--tpcomm", default="auto")
     ap.add_argument("--out", default="")
     # arguments come through MP_WORKER_ARGS: torchrun's own parser would
     # otherwise claim any option that prefixes one of its flags (--m, --t ...)
@@ -53,7 +54,7 @@ def main():
     W = gen.model_weights(shape, seed=42, dtype=a.dtype)
     tok = gen.tokens(a.m, shape.s, shape.V, seed=1234)
     cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype, attn=a.attn,
-                      p_drop_attn=a.pdrop, p_drop_hidden=a.pdrop, seed=4321)
+                      p_drop_attn=a.pdrop, p_drop_hidden=a.pdrop, seed=4321, tp_comm=a.tpcomm)
     ctx = mp.Context(a.t, a.p, a.v, 1, cfg, rank, world, local, nid[0])
     tp, pp = rank % a.t, (rank // a.t) % a.p
     tol = {"bf16": 2e-2, "fp32": 1e-4}[a.dtype]
@@ -73,6 +74,7 @@ def main():
         lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m, masks=masks)
         report["loss"] = [loss, lr]
         report["stats"] = stats
+        report["tp_comm"] = ctx.tp_comm_mode()
         ok = abs(loss - lr) / abs(lr) < tol
         dev_of, _ = mp.mp_get_stage_map(shape.l, a.p, a.v)
 

@@ -94,3 +94,28 @@ def test_multi_gpu_parity_dropout(tmp_path, t, p, v, m, sched, attn):
     msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
     assert r.returncode == 0, msg
     assert len(reps) == n and all(x["ok"] for x in reps), msg
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("tpcomm", ["nccl", "nvls"])
+@pytest.mark.parametrize("t,p,v,m,sched", [(2, 1, 1, 4, "1f1b"), (4, 1, 1, 4, "1f1b"), (2, 2, 2, 4, "interleaved")])
+def test_multi_gpu_tp_transport(tmp_path, t, p, v, m, sched, tpcomm, dtype):
+    """Both transports of the g / f all-reduces give the oracle's results: the
+    paper's NCCL all-reduce and the NVLS reduce-load fused into the consuming
+    LayerNorm / residual kernels (required here: fails if multicast is absent)."""
+    n = t * p
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = str(tmp_path / "rep")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={35000 + (hash((t, p, v, m, sched, tpcomm, dtype)) % 2000)}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype {dtype} "
+                                          f"--tpcomm {tpcomm} --out {out}")
+    env.pop("MP_TP_COMM", None)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
+    msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
+    assert r.returncode == 0, msg
+    assert len(reps) == n and all(x["ok"] for x in reps), msg
+    assert all(x.get("tp_comm") == tpcomm for x in reps), msg
