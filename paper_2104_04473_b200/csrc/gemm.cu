@@ -424,7 +424,14 @@ static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, 
   return launch_tc<BN, true, true>(ta, tb, tc, a, grid, st);
 }
 
-static int tc_grid(const TcArgs& a) { return std::max(1, std::min(a.num_tiles, num_sms())); }
+// CTA budget of the next persistent GEMM launches (0 = every SM): lets a GEMM
+// on a side stream leave SMs to a concurrent communication-bound kernel.
+static int g_max_ctas = 0;
+void gemm_set_max_ctas(int n) { g_max_ctas = n; }
+static int tc_grid(const TcArgs& a) {
+  const int cap = g_max_ctas > 0 ? std::min(g_max_ctas, num_sms()) : num_sms();
+  return std::max(1, std::min(a.num_tiles, cap));
+}
 
 mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return set_err(MP_EINVAL, "gemm: empty shape");

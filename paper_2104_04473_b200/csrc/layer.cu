@@ -75,14 +75,16 @@ static mp_status lin_dgrad(mp_ctx* c, const void* dY, const void* W, void* dX, i
   g.c_fp32 = c->cfg.dtype == MP_FP32;
   return gemm(c->cfg.dtype, g, c->cs);
 }
+void gemm_set_max_ctas(int n);
 // dW[N, K] += dY[T, N]^T X[T, K]  (fp32 accumulators)
-static mp_status lin_wgrad(mp_ctx* c, const void* dY, const void* X, float* dW, int T, int N, int K) {
+static mp_status lin_wgrad(mp_ctx* c, const void* dY, const void* X, float* dW, int T, int N, int K,
+                           cudaStream_t st = nullptr) {
   mp_gemm_desc g{};
   g.M = N; g.N = K; g.K = T; g.batch = 1;
   g.A = dY; g.lda = N; g.a_major = 1;
   g.B = X; g.ldb = K; g.b_major = 1;
   g.C = dW; g.ldc = K; g.c_fp32 = 1; g.accumulate = 1; g.alpha = 1.f;
-  return gemm(c->cfg.dtype, g, c->cs);
+  return gemm(c->cfg.dtype, g, st ? st : c->cs);
 }
 
 template <class T> static T* ptr(mp_ctx* c, int pidx) {
@@ -277,6 +279,13 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
   return MP_OK;
 }
 
+// SMs the side-stream dW GEMM may use while the NVLS LayerNorm backward runs
+// (MP_WGRAD_SM_RESERVE SMs are left to it; default 0 = share every SM).
+static int wgrad_ctas() {
+  static const int reserve = getenv("MP_WGRAD_SM_RESERVE") ? atoi(getenv("MP_WGRAD_SM_RESERVE")) : 0;
+  return reserve > 0 ? std::max(1, num_sms() - reserve) : 0;
+}
+
 template <class T>
 static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const void* dy, void* dx) {
   const Dims d = dims(c, st.b);
@@ -307,15 +316,25 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   if (nv) tp_sym_next(c, &fw, &fr);
   if (nv && !nvr) fr = fw;
   MP_TRY(lin_dgrad(c, dU, ptr<T>(c, lp[P_W1]), fw, d.T, d.h4t, d.h));
-  if (c->t > 1 && !nv) {
+  if (c->t > 1) {
+    // the f all-reduce (NCCL) or the barrier + reduce-loading LayerNorm backward (NVLS) overlaps dW1
     MP_CUDA(cudaEventRecord(ev_a, c->cs));
     MP_CUDA(cudaStreamWaitEvent(c->side, ev_a, 0));
+  }
+  if (c->t > 1 && !nv) {
     MP_TRY(allreduce(c, dA2, (size_t)d.T * d.h, c->side));
     MP_CUDA(cudaEventRecord(ev_b, c->side));
+    MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
+    MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
+  } else if (nv) {
+    gemm_set_max_ctas(wgrad_ctas());
+    MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h, c->side));
+    gemm_set_max_ctas(0);
+    MP_CUDA(cudaEventRecord(ev_b, c->side));
+    MP_TRY(tp_sym_barrier(c, c->cs));
+  } else {
+    MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
   }
-  MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
-  if (c->t > 1 && !nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
-  if (nv) MP_TRY(tp_sym_barrier(c, c->cs));
   MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
                           gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs,
                           nvr ? dA2 : nullptr));
@@ -327,6 +346,7 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   } else {
     MP_TRY(colsum_accum<T>(dX1, gptr(c, lp[P_BO]), d.T, d.h, c->cs));
   }
+  if (nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));   // dW1 done before dU / A2 are reused
   MP_TRY(lin_dgrad(c, dZ1, ptr<T>(c, lp[P_WO]), c->ws_dctx, d.T, d.h, d.ht));
   MP_TRY(lin_wgrad(c, dZ1, st.ctx, gptr(c, lp[P_WO]), d.T, d.h, d.ht));
   if (use_fused(c))
@@ -340,18 +360,28 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   if (nv) tp_sym_next(c, &fw, &fr);
   if (nv && !nvr) fr = fw;
   MP_TRY(lin_dgrad(c, c->ws_dqkv, ptr<T>(c, lp[P_WQKV]), fw, d.T, d.h3t, d.h));
-  if (c->t > 1 && !nv) {
+  if (c->t > 1) {
     MP_CUDA(cudaEventRecord(ev_a, c->cs));
     MP_CUDA(cudaStreamWaitEvent(c->side, ev_a, 0));
+  }
+  if (c->t > 1 && !nv) {
     MP_TRY(allreduce(c, dA, (size_t)d.T * d.h, c->side));
     MP_CUDA(cudaEventRecord(ev_b, c->side));
+    MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
+    MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
+  } else if (nv) {
+    gemm_set_max_ctas(wgrad_ctas());
+    MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h, c->side));
+    gemm_set_max_ctas(0);
+    MP_CUDA(cudaEventRecord(ev_b, c->side));
+    MP_TRY(tp_sym_barrier(c, c->cs));
+  } else {
+    MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
   }
-  MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
-  if (c->t > 1 && !nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));
-  if (nv) MP_TRY(tp_sym_barrier(c, c->cs));
   MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.x, ptr<T>(c, lp[P_LN1G]), st.mu1, st.rs1, dX1, (T*)dx,
                           gptr(c, lp[P_LN1G]), gptr(c, lp[P_LN1B]), c->ws_ln, d.T, d.h, c->cs,
                           nvr ? dA : nullptr));
+  if (nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));   // dWqkv done before the stash is released
   return MP_OK;
 }
 
