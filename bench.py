@@ -29,6 +29,16 @@ import time
 
 import numpy as np
 
+# stdout carries exactly one JSON line: library chatter (e.g. NCCL's version
+# banner printed from C) is sent to stderr, the JSON goes to the saved stdout
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(obj):
+    sys.stdout.flush()
+    os.write(_JSON_FD, (json.dumps(obj) + "\n").encode())
+
 # Enough hardware work queues that the compute stream's waits on P2P events
 # never sit in front of a channel stream's NCCL kernel (false dependencies
 # deadlock the pipeline otherwise).  Must be set before CUDA initialises.
@@ -180,7 +190,7 @@ def run_reference(args, cfg, world, rank):
            "data": "synthetic", "config": workload_config(args, cfg),
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(out), flush=True)
+    emit(out)
 
 
 def replay_bubble(p, m, v, sched, tf, tb):
@@ -386,7 +396,7 @@ def main():
         "metric": METRIC, "value": agg, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
-        "config": dict(workload_config(args, cfg), tp_comm=ctx.tp_comm_mode()),
+        "config": dict(workload_config(args, cfg), tp_comm=ctx.tp_comm_mode() if t > 1 else "none (t=1)"),
         "per_gpu_tflops": per_gpu,
         "pct_of_bf16_peak": {"measured_burst_1683": 100 * per_gpu / pk["bf16_burst"],
                              "measured_sustained": 100 * per_gpu / pk["bf16_sustained"],
@@ -414,7 +424,7 @@ def main():
                                "sample": f"one unpartitioned GPT-{args.model} layer fwd+bwd (b=1, s={cfg.s}), "
                                          f"fp64 numpy oracle, {f:.3g} FLOP"}
     if rank == 0:
-        print(json.dumps(out), flush=True)
+        emit(out)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()

@@ -98,9 +98,11 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // heaviest (longest causal range) query tiles first
-  const int qt = g.nq - 1 - (int)(blockIdx.x % g.nq);
-  const int z = (int)(blockIdx.x / g.nq);
+  // heaviest (longest causal range) query tiles first across the whole grid
+  // (longest-processing-time-first list scheduling of the CTAs onto the SMs)
+  const int zn = (int)(gridDim.x / g.nq);
+  const int qt = g.nq - 1 - (int)(blockIdx.x / zn);
+  const int z = (int)(blockIdx.x % zn);
   const int nkv = qt + 1;
 
   if (threadIdx.x == 0) {
@@ -375,8 +377,10 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int kt = (int)(blockIdx.x % g.nq);         // key/value tile
-  const int z = (int)(blockIdx.x / g.nq);
+  // key/value tile, heaviest (most query tiles) first across the whole grid
+  const int zn = (int)(gridDim.x / g.nq);
+  const int kt = (int)(blockIdx.x / zn);
+  const int z = (int)(blockIdx.x % zn);
   const int niter = g.nq - kt;                      // query tiles kt .. nq-1
   const int tile_bytes = g.nhb * 128 * 128;
 

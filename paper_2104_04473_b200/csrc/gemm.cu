@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -56,6 +57,8 @@ struct TcArgs {
   const __nv_bfloat16* bias;
   int c_fp32, accumulate, causal, vec_ok;
   int tma_out;          // epilogue through shared memory + TMA store / reduce-add (tmC valid)
+  int stream_k;         // accumulate mode: CTAs split the (tile, k-block) iterations evenly
+  int kb_per_tile;      // k-blocks per tile (stream_k)
   float alpha;
 };
 
@@ -69,6 +72,49 @@ __device__ __forceinline__ void k_range(const TcArgs& g, int m_blk, int& kb0, in
   if (g.causal == 3) kb0 = (m_blk * BM) / BK;
   kb1 = (kend + BK - 1) / BK;
 }
+
+// Work sequence of one CTA, identical for the producer, MMA and epilogue roles.
+// Tile mode: tiles blockIdx.x, +gridDim.x, ... with their (causal) k-block ranges.
+// Stream-K mode (accumulate GEMMs, whose epilogue is a TMA reduce-add into the
+// fp32 accumulator): the num_tiles * kb_per_tile (tile, k-block) iterations are
+// cut into gridDim.x equal contiguous ranges, so every SM gets the same number
+// of k-blocks (no partial last wave); a tile split between CTAs is simply
+// reduce-added twice.
+struct WorkIter {
+  long long i, i1;
+  int t;
+  __device__ __forceinline__ explicit WorkIter(const TcArgs& g) {
+    if (g.stream_k) {
+      const long long I = (long long)g.num_tiles * g.kb_per_tile;
+      i = I * blockIdx.x / gridDim.x;
+      i1 = I * (blockIdx.x + 1) / gridDim.x;
+    }
+    t = blockIdx.x;
+  }
+  template <int BN>
+  __device__ __forceinline__ bool next(const TcArgs& g, int& tile, int& kb0, int& kb1) {
+    if (g.stream_k) {
+      if (i >= i1) return false;
+      tile = (int)(i / g.kb_per_tile);
+      kb0 = (int)(i % g.kb_per_tile);
+      const long long e = min(i1, (long long)(tile + 1) * g.kb_per_tile);
+      kb1 = kb0 + (int)(e - i);
+      i = e;
+      return true;
+    }
+    const int tiles_per_batch = g.m_blocks * g.n_blocks;
+    while (t < g.num_tiles) {
+      tile = t;
+      t += gridDim.x;
+      const int rem = tile % tiles_per_batch;
+      const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+      if (tile_skipped(g, m_blk, n_blk, BN)) continue;
+      k_range(g, m_blk, kb0, kb1);
+      return true;
+    }
+    return false;
+  }
+};
 
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -111,11 +157,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
       int stage = 0; uint32_t phase = 0;
-      for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
+      WorkIter it(g);
+      int t, kb0, kb1;
+      while (it.next<BN>(g, t, kb0, kb1)) {
         const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
         const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
-        if (tile_skipped(g, m_blk, n_blk, BN)) continue;
-        int kb0, kb1; k_range(g, m_blk, kb0, kb1);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
@@ -145,11 +191,9 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
-        const int rem = t % tiles_per_batch;
-        const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
-        if (tile_skipped(g, m_blk, n_blk, BN)) continue;
-        int kb0, kb1; k_range(g, m_blk, kb0, kb1);
+      WorkIter it(g);
+      int t, kb0, kb1;
+      while (it.next<BN>(g, t, kb0, kb1)) {
         mbar_wait(&tempty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
@@ -183,11 +227,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int half = (warp - 2) / 4;         // the two warps of a quarter take alternate column boxes
     int acc = 0; uint32_t acc_phase = 0;
     uint8_t* stage_base = sOut + (warp - 2) * 4096;
-    for (int t = blockIdx.x; t < g.num_tiles; t += gridDim.x) {
+    WorkIter it(g);
+    int t, kb0, kb1;
+    while (it.next<BN>(g, t, kb0, kb1)) {
       const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
       const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
-      if (tile_skipped(g, m_blk, n_blk, BN)) continue;
-      int kb0, kb1; k_range(g, m_blk, kb0, kb1);
       const bool have_acc = kb1 > kb0;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -428,9 +472,21 @@ static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, 
 // on a side stream leave SMs to a concurrent communication-bound kernel.
 static int g_max_ctas = 0;
 void gemm_set_max_ctas(int n) { g_max_ctas = n; }
+static int sm_cap() { return g_max_ctas > 0 ? std::min(g_max_ctas, num_sms()) : num_sms(); }
 static int tc_grid(const TcArgs& a) {
-  const int cap = g_max_ctas > 0 ? std::min(g_max_ctas, num_sms()) : num_sms();
-  return std::max(1, std::min(a.num_tiles, cap));
+  if (a.stream_k) return sm_cap();
+  return std::max(1, std::min(a.num_tiles, sm_cap()));
+}
+// Stream-K for an accumulate GEMM when whole-tile scheduling would leave the
+// last wave less than ~90% full and every CTA still gets >= 8 k-blocks.
+static bool want_stream_k(const TcArgs& a) {
+  if (!a.accumulate || !a.tma_out || a.bias || a.causal) return false;
+  const int G = sm_cap();
+  if (a.num_tiles <= 0) return false;
+  const long long waves = (a.num_tiles + G - 1) / G;
+  const double fill = (double)a.num_tiles / (double)(waves * G);
+  const long long iters = (long long)a.num_tiles * a.kb_per_tile;
+  return fill < 0.9 && iters / G >= 8;
 }
 
 mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
@@ -461,6 +517,10 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   memset(&tc, 0, sizeof(tc));
   // epilogue via TMA: C box = 32 rows x 128 bytes
   a.tma_out = a.vec_ok && make_map(&tc, g.C, g.N, g.M, g.batch, g.ldc, g.strideC, 32, esz);
+  a.kb_per_tile = (g.K + BK - 1) / BK;
+  a.stream_k = 0;
+  static const bool no_sk = getenv("MP_GEMM_NO_STREAMK") != nullptr;
+  a.stream_k = want_stream_k(a) && !no_sk;
   const int grid = tc_grid(a);
   cudaError_t e;
   if (BN == 64) e = dispatch_major<64>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);

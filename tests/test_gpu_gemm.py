@@ -141,3 +141,13 @@ def test_gemm_attention_layout(dtype, s, b, heads, hd):
             assert normwise(host(S[zz]), Sr) < 1e-4, (bb, j)
             Cr = P[zz] @ Q4[:, bb, j, 2]
             assert normwise(host(ctx[:, bb, j]), Cr) < 1e-4, (bb, j)
+
+
+@pytest.mark.parametrize("am,bm", [(1, 1), (0, 1)])
+@pytest.mark.parametrize("M,N,K", [(2304, 2304, 2048), (1000, 1304, 2048), (768, 2304, 4096)])
+def test_gemm_bf16_stream_k_accumulate(am, bm, M, N, K):
+    """Weight-gradient-shaped accumulate GEMMs whose tile count leaves the last
+    wave mostly empty: the (tile, k-block) iterations are split evenly across
+    the SMs and partial tiles are reduce-added into the fp32 accumulator."""
+    got, ref = run_gemm(M, N, K, 1, am, bm, c_fp32=True, accumulate=True)
+    assert normwise(got, ref) < 1e-4
