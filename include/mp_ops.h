@@ -122,7 +122,10 @@ mp_status mp_op_flash_attn_fwd(const void* qkv, void* ctx, float* lse2, int s, i
 
 /* Backward of mp_op_flash_attn_fwd: writes dQ, dK, dV into the q/k/v slots of
  * dqkv (bf16, same layout as qkv) from qkv, ctx, dctx and lse2; ws is an fp32
- * workspace of mp_op_flash_attn_bwd_ws_floats(s, b, heads, hd) floats. */
+ * workspace of mp_op_flash_attn_bwd_ws_floats(s, b, heads, hd) floats (dQ
+ * accumulator, D = rowsum(dO o O), and the dK / dV accumulators used when the
+ * kernel splits each key tile's query range over several CTAs to fill the SMs
+ * at small b * heads).  dK / dV accumulation order then varies run to run. */
 long long mp_op_flash_attn_bwd_ws_floats(int s, int b, int heads, int hd);
 mp_status mp_op_flash_attn_bwd(const void* qkv, const void* ctx, const void* dctx, const float* lse2, void* dqkv,
                                float* ws, int s, int b, int heads, int hd, void* stream);

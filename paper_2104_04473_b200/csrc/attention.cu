@@ -22,6 +22,12 @@
 #include <cfloat>
 #include <cmath>
 #include <cstring>
+#include <algorithm>
+#include <functional>
+#include <map>
+#include <queue>
+#include <tuple>
+#include <vector>
 
 #include "common.h"
 #include "ptx.cuh"
@@ -62,6 +68,9 @@ struct FaArgs {
   float scale_log2;
   Dropout dp;                  // attention-probability dropout (off when dp.thresh == 0)
   long long* trace;            // debug: per-tile event timestamps of CTA 0 (null = off)
+  const int4* work;            // split-KV mode: per CTA ((z << 16) | q tile, first kv tile, end kv tile, slot)
+  float* Opart;                // split-KV: unnormalised fp32 O [slot][128][hd]
+  float2* ml;                  // split-KV: (reference max m, sum l) [slot][128]
 };
 
 __device__ __forceinline__ long long gtime() {
@@ -99,11 +108,18 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // heaviest (longest causal range) query tiles first across the whole grid
-  // (longest-processing-time-first list scheduling of the CTAs onto the SMs)
-  const int zn = (int)(gridDim.x / g.nq);
-  const int qt = g.nq - 1 - (int)(blockIdx.x / zn);
-  const int z = (int)(blockIdx.x % zn);
-  const int nkv = qt + 1;
+  // (longest-processing-time-first list scheduling of the CTAs onto the SMs);
+  // split-KV mode: the CTA covers kv tiles j0 .. j0+nkv-1 of its query tile
+  int qt, z, j0 = 0, nkv, slot = -1;
+  if (g.work) {
+    const int4 w = g.work[blockIdx.x];
+    z = w.x >> 16; qt = w.x & 0xffff; j0 = w.y; nkv = w.z - w.y; slot = w.w;
+  } else {
+    const int zn = (int)(gridDim.x / g.nq);
+    qt = g.nq - 1 - (int)(blockIdx.x / zn);
+    z = (int)(blockIdx.x % zn);
+    nkv = qt + 1;
+  }
 
   if (threadIdx.x == 0) {
     mbar_init(q_full, 1);
@@ -133,14 +149,15 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         if (j >= 2) mbar_wait(&kv_empty[st], ((j >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&k_full[st], g.nhb * BKV * 128);
         for (int hb = 0; hb < g.nhb; ++hb)
-          tma_load_3d(sK + st * K_BYTES + hb * BKV * 128, &tmK, &k_full[st], 64 * hb, j * BKV, z);
+          tma_load_3d(sK + st * K_BYTES + hb * BKV * 128, &tmK, &k_full[st], 64 * hb, (j0 + j) * BKV, z);
         FA_TRACE(0, j);
         if (j >= 2) mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
         FA_TRACE(1, j);
         mbar_arrive_expect_tx(&v_full[st], g.nhb * 2 * 64 * 128);
         for (int hb = 0; hb < g.nhb; ++hb)
           for (int kb = 0; kb < 2; ++kb)
-            tma_load_3d(sV + st * V_BYTES + hb * 2 * 8192 + kb * 8192, &tmV, &v_full[st], 64 * hb, j * BKV + 64 * kb, z);
+            tma_load_3d(sV + st * V_BYTES + hb * 2 * 8192 + kb * 8192, &tmV, &v_full[st], 64 * hb,
+                        (j0 + j) * BKV + 64 * kb, z);
       }
     }
   } else if (warp == 1) {
@@ -196,7 +213,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const int sb = j & 1;
       mbar_wait(&s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      const bool diag = j == qt;
+      const bool diag = j0 + j == qt;
       const uint32_t sa = tmem + lane_off + sb * 128;
       // the whole S row (128 fp32) into registers with one wait; the TMEM tile is then free
       uint32_t sv[128];
@@ -251,7 +268,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         uint32_t km = 0xffffffffu;
         if (drop) {
           km = 0;
-          const unsigned long long e0 = (unsigned long long)qrow * g.s + j * BKV + 32 * c;
+          const unsigned long long e0 = (unsigned long long)qrow * g.s + (j0 + j) * BKV + 32 * c;
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4)
             km |= keep4(g.dp, e0 / 4 + q4, g.dp.head0 + zj, g.dp.seq0 + zb) << (4 * q4);
@@ -291,6 +308,21 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     // epilogue: O / l -> bf16 context row, L2 = m + log2(l)
     mbar_wait(&pv_done[(nkv - 1) & 1], ((nkv - 1) >> 1) & 1);
     tc_fence_after();
+    if (g.work) {
+      // partial result of kv tiles j0 .. j0+nkv-1: unnormalised O, reference max, sum
+      // layout [slot][hd / 4][128 rows] of float4: a warp's stores are contiguous
+      float4* op = reinterpret_cast<float4*>(g.Opart) + (long long)slot * (g.hd / 4) * BQ + r;
+      for (int c = 0; c < g.hd; c += 32) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + 256 + c, o);
+        tmem_ld_wait();
+#pragma unroll
+        for (int q4 = 0; q4 < 8; ++q4)
+          op[(c / 4 + q4) * BQ] = make_float4(__uint_as_float(o[4 * q4]), __uint_as_float(o[4 * q4 + 1]),
+                                              __uint_as_float(o[4 * q4 + 2]), __uint_as_float(o[4 * q4 + 3]));
+      }
+      g.ml[(long long)slot * BQ + r] = make_float2(m, l);
+    } else {
     const float inv = 1.f / l;
     const bool ok = qrow < g.s;
     __nv_bfloat16* orow = g.O + (long long)qrow * g.ldo + (long long)z * g.hd;
@@ -314,6 +346,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
     }
     if (ok) g.L2[(long long)z * g.s + qrow] = m + log2f(l);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -331,6 +364,10 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 // as K-major and (via the MN-major descriptor view) MN-major operands, and P
 // / dS as K-major (dQ) and MN-major (dV, dK) operands: no transposes.
 namespace fab {
+// warp 0 TMA, warp 1 MMA, warps 2-9 compute: two warps per TMEM lane quarter,
+// each taking half of the 128 key columns (P / dS) and of the dQ chunks
+constexpr int THREADS = 320;
+constexpr int CW = 256;                      // compute threads
 constexpr int T_BYTES = 2 * 128 * 128;       // one [128 rows x hd<=128] bf16 tile (2 hd blocks)
 constexpr int SMEM = 6 * T_BYTES + 1024 + 512;
 }  // namespace fab
@@ -345,6 +382,9 @@ struct FabArgs {
   float scale_log2, scale;
   Dropout dp;
   long long* trace;
+  const int4* work;    // split mode: per CTA (z, kv tile, first, end query-tile offset); null = whole ranges
+  float* dKacc;        // split mode: fp32 [z, s, hd] accumulators of dK / dV (zeroed)
+  float* dVacc;
 };
 
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c, float d) {
@@ -353,7 +393,7 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 }
 
 template <bool DROP>
-__global__ void __launch_bounds__(fa::THREADS, 1)
+__global__ void __maxnreg__(168)
 flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                  const __grid_constant__ CUtensorMap tmdQ, FabArgs g) {
@@ -377,16 +417,23 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // key/value tile, heaviest (most query tiles) first across the whole grid
-  const int zn = (int)(gridDim.x / g.nq);
-  const int kt = (int)(blockIdx.x / zn);
-  const int z = (int)(blockIdx.x % zn);
-  const int niter = g.nq - kt;                      // query tiles kt .. nq-1
+  // key/value tile, heaviest (most query tiles) first across the whole grid;
+  // split mode: a CTA takes query tiles kt+it0 .. kt+it1-1 of its kv tile
+  int kt, z, it0 = 0, niter;
+  if (g.work) {
+    const int4 w = g.work[blockIdx.x];
+    z = w.x; kt = w.y; it0 = w.z; niter = w.w - w.z;
+  } else {
+    const int zn = (int)(gridDim.x / g.nq);
+    kt = (int)(blockIdx.x / zn);
+    z = (int)(blockIdx.x % zn);
+    niter = g.nq - kt;                              // query tiles kt .. nq-1
+  }
   const int tile_bytes = g.nhb * 128 * 128;
 
   if (threadIdx.x == 0) {
     mbar_init(kv_full, 1); mbar_init(qd_full, 1); mbar_init(qd_empty, 1); mbar_init(sdp_full, 1);
-    mbar_init(ds_ready, 128); mbar_init(dq_full, 1); mbar_init(tmem_free, 128);
+    mbar_init(ds_ready, CW); mbar_init(dq_full, 1); mbar_init(tmem_free, CW);
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -406,7 +453,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         tma_load_3d(sV + hb * 16384, &tmV, kv_full, 64 * hb, kt * 128, z);
       }
       for (int it = 0; it < niter; ++it) {
-        const int qi = kt + it;
+        const int qi = kt + it0 + it;
         if (it > 0) mbar_wait(qd_empty, (it - 1) & 1);
         mbar_arrive_expect_tx(qd_full, 2 * tile_bytes);
         for (int hb = 0; hb < g.nhb; ++hb) {
@@ -459,15 +506,16 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     }
   } else {
     const int quarter = warp % 4;
+    const int half = (warp - 2) / 4;               // key columns 64 half .. +63, dQ chunks c0 + half
     const int r = quarter * 32 + lane;
     const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
     float l2n = 0.f, ddn = 0.f;
     {
-      const int q0 = kt * 128 + r;
+      const int q0 = (kt + it0) * 128 + r;
       if (q0 < g.s) { l2n = g.L2[(long long)z * g.s + q0]; ddn = g.D[(long long)z * g.s + q0]; }
     }
     for (int it = 0; it < niter; ++it) {
-      const int qi = kt + it;
+      const int qi = kt + it0 + it;
       const int q = qi * 128 + r;
       const bool qok = q < g.s;
       const float l2 = l2n, dd = ddn;
@@ -475,7 +523,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         l2n = g.L2[(long long)z * g.s + q + 128];
         ddn = g.D[(long long)z * g.s + q + 128];
       }
-      const bool diag = it == 0;
+      const bool diag = qi == kt;
       mbar_wait(sdp_full, it & 1);
       tc_fence_after();
       if (threadIdx.x == 64) FA_TRACE(3, it);
@@ -483,7 +531,8 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       constexpr bool drop = DROP;
       const int zb = z / g.dp.heads, zj = z % g.dp.heads;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int cc = 0; cc < 2; ++cc) {
+        const int c = 2 * half + cc;
         uint32_t sv[32], dv[32];
         tmem_ld_32x32b_x32(tmem + lane_off + 32 * c, sv);
         tmem_ld_32x32b_x32(tmem + lane_off + 128 + 32 * c, dv);
@@ -535,32 +584,31 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tc_fence_after();
       if (threadIdx.x == 64) FA_TRACE(5, it);
       const int nchunk = g.hd / 32;
-      const uint32_t stg = smem_u32(sP);
+      const uint32_t stg = smem_u32(sP) + half * 16384;
       for (int c0 = 0; c0 < nchunk; c0 += 2) {
-        uint32_t dqv[2][32];
-#pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (c0 + u < nchunk) tmem_ld_32x32b_x32(tmem + lane_off + 128 + 32 * (c0 + u), dqv[u]);
-        tmem_ld_wait();
+        const int c = c0 + half;
+        const bool has = c < nchunk;                 // warp-uniform
+        uint32_t dqv[32];
+        if (has) {
+          tmem_ld_32x32b_x32(tmem + lane_off + 128 + 32 * c, dqv);
+          tmem_ld_wait();
+        }
         if (c0 + 2 >= nchunk) {
           tc_fence_before();
           mbar_arrive(tmem_free);      // the next S / dP products may now overwrite TMEM
         }
-        if (c0 >= 2) {                 // boxes c0-2, c0-1 (same staging halves) must have been read
+        if (c0 >= 2) {                 // the previous boxes (same staging halves) must have been read
           if (threadIdx.x == 64) bulk_wait_read<0>();
-          named_bar_sync(1, 128);
+          named_bar_sync(1, CW);
         }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          if (c0 + u >= nchunk) break;
-          const uint32_t rowa = stg + u * 16384 + r * 128;
+        if (has) {
+          const uint32_t rowa = stg + r * 128;
 #pragma unroll
           for (int j = 0; j < 8; ++j)
-            st_shared_v4(rowa + ((j ^ (r & 7)) << 4), dqv[u][4 * j], dqv[u][4 * j + 1], dqv[u][4 * j + 2],
-                         dqv[u][4 * j + 3]);
+            st_shared_v4(rowa + ((j ^ (r & 7)) << 4), dqv[4 * j], dqv[4 * j + 1], dqv[4 * j + 2], dqv[4 * j + 3]);
         }
         fence_proxy_async_smem();
-        named_bar_sync(1, 128);
+        named_bar_sync(1, CW);
         if (threadIdx.x == 64) {
           for (int u = 0; u < 2 && c0 + u < nchunk; ++u)
             tma_reduce_add_3d(&tmdQ, sP + u * 16384, 32 * (c0 + u), qi * 128, z);
@@ -569,7 +617,7 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
       // the P tile is rewritten by the next iteration: wait until the TMA has read it
       if (threadIdx.x == 64) bulk_wait_read<0>();
-      named_bar_sync(1, 128);
+      named_bar_sync(1, CW);
       if (threadIdx.x == 64) FA_TRACE(6, it);
     }
     if (threadIdx.x == 64) bulk_wait_all();
@@ -581,8 +629,23 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const int zb = z / g.heads, zh = z % g.heads;
       (void)zb; (void)zh;
       __nv_bfloat16* base = g.dQKV + (long long)kvrow * g.ldq + (long long)z * 3 * g.hd;
-      for (int part = 0; part < 2; ++part) {          // 0: dK (cols 384), 1: dV (cols 256)
-        const uint32_t col0 = part == 0 ? 384 : 256;
+      const int part = half;                            // 0: dK (cols 384), 1: dV (cols 256)
+      const uint32_t col0 = part == 0 ? 384 : 256;
+      if (g.work) {
+        // partial sums over this CTA's query tiles: fp32 reductions into the accumulators
+        float* acc = (part == 0 ? g.dKacc : g.dVacc) + ((long long)z * g.s + kvrow) * g.hd;
+        for (int c = 0; c < g.hd; c += 32) {
+          uint32_t v[32];
+          tmem_ld_32x32b_x32(tmem + lane_off + col0 + c, v);
+          tmem_ld_wait();
+          if (ok) {
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4)
+              red_add_v4(acc + c + 4 * q4, __uint_as_float(v[4 * q4]), __uint_as_float(v[4 * q4 + 1]),
+                         __uint_as_float(v[4 * q4 + 2]), __uint_as_float(v[4 * q4 + 3]));
+          }
+        }
+      } else {
         __nv_bfloat16* dst = base + (part == 0 ? g.hd : 2 * g.hd);
         for (int c = 0; c < g.hd; c += 32) {
           uint32_t v[32];
@@ -632,8 +695,11 @@ __global__ void flash_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO, const
 }
 
 // dQacc fp32 [z, s, hd] -> bf16 Q slot of dQKV [s, b, heads, 3, hd]
-__global__ void flash_bwd_dq_kernel(const float* __restrict__ acc, __nv_bfloat16* __restrict__ dQKV, int s, int zn,
-                                    int hd, long long ldq) {
+// (dQ: slot 0; split mode also dK: slot 1, dV: slot 2)
+__global__ void flash_bwd_dq_kernel(const float* __restrict__ acc0, __nv_bfloat16* __restrict__ dQKV, int s, int zn,
+                                    int hd, long long ldq, int slot0, long long slot_stride) {
+  const int slot = slot0 + (int)blockIdx.y;        // destination slot; accumulators slot_stride floats apart
+  const float* acc = acc0 + blockIdx.y * slot_stride;
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;   // one pair of elements
   const long long n = (long long)zn * s * hd / 2;
   if (i >= n) return;
@@ -642,7 +708,66 @@ __global__ void flash_bwd_dq_kernel(const float* __restrict__ acc, __nv_bfloat16
   const long long zq = e / hd;
   const int q = (int)(zq % s), z = (int)(zq / s);
   const float2 v = *reinterpret_cast<const float2*>(acc + e);
-  *reinterpret_cast<__nv_bfloat162*>(dQKV + (long long)q * ldq + (long long)z * 3 * hd + d) = __floats2bfloat162_rn(v.x, v.y);
+  *reinterpret_cast<__nv_bfloat162*>(dQKV + (long long)q * ldq + (long long)z * 3 * hd + slot * hd + d) =
+      __floats2bfloat162_rn(v.x, v.y);
+}
+
+// Split-Q work decomposition of the backward (few heads per rank, e.g. t >= 2):
+// a kv tile's query range [kt, nq) is cut into chunks of L tiles so that the
+// grid fills the SMs; L is chosen by list-scheduling the CTAs (heaviest
+// first) onto the SMs under a cost model of one unit per query tile plus
+// per-CTA overheads, against the unsplit decomposition.  Cached per shape.
+struct BwdWork { int4* dev = nullptr; int n = 0; };
+static double makespan(std::vector<double> jobs, int M) {
+  std::sort(jobs.begin(), jobs.end(), std::greater<double>());
+  std::priority_queue<double, std::vector<double>, std::greater<double>> h;
+  for (int i = 0; i < M; ++i) h.push(0.0);
+  double mx = 0;
+  for (double j : jobs) { double t = h.top(); h.pop(); t += j; mx = std::max(mx, t); h.push(t); }
+  return mx;
+}
+static const BwdWork* bwd_work(int zn, int nq, cudaStream_t st) {
+  static std::map<std::pair<int, int>, BwdWork> cache;
+  auto key = std::make_pair(zn, nq);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second.dev ? &it->second : nullptr;
+  const int M = num_sms();
+  auto jobs_for = [&](int L) {
+    std::vector<double> j;
+    for (int z = 0; z < zn; ++z)
+      for (int kt = 0; kt < nq; ++kt)
+        for (int c = 0; c < nq - kt; c += L) j.push_back(std::min(L, nq - kt - c) + 0.5 + (L < nq ? 0.3 : 0.0));
+    return j;
+  };
+  int bestL = nq;
+  double best = makespan(jobs_for(nq), M);
+  for (int L : {8, 6, 5, 4, 3, 2}) {
+    if (L >= nq) continue;
+    const double m = makespan(jobs_for(L), M) + 1.5;   // + zeroing / converting the dK, dV accumulators
+    if (m < 0.85 * best) { best = m; bestL = L; }
+  }
+  if (const char* e = getenv("MP_FA_BWD_SPLIT_L")) bestL = std::max(1, std::min(nq, atoi(e)));   // tuning sweeps
+  BwdWork w;
+  if (bestL < nq) {
+    std::vector<int4> items;
+    for (int z = 0; z < zn; ++z)
+      for (int kt = 0; kt < nq; ++kt)
+        for (int c = 0; c < nq - kt; c += bestL) items.push_back(make_int4(z, kt, c, std::min(nq - kt, c + bestL)));
+    std::stable_sort(items.begin(), items.end(), [](const int4& a, const int4& b) { return a.w - a.z > b.w - b.z; });
+    if (cudaMalloc(&w.dev, items.size() * sizeof(int4)) == cudaSuccess &&
+        cudaMemcpy(w.dev, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice) == cudaSuccess)
+      w.n = (int)items.size();
+    else
+      w.dev = nullptr;
+  }
+  (void)st;
+  auto& ref = cache[key] = w;
+  return ref.dev ? &ref : nullptr;
+}
+
+long long flash_bwd_ws_floats(int s, int b, int heads, int hd) {
+  // dQ accumulator, D, and (split mode) dK / dV accumulators
+  return (long long)b * heads * s * (3LL * hd + 1);
 }
 
 // dQKV = d/dQKV of the fused attention, given O (= ctx), dO (= dctx), L2 from the forward.
@@ -662,7 +787,12 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   if (!ok) return set_err(MP_ECUDA, "flash attention bwd: tensor map encode failed");
   float* dqacc = ws;
   float* D = ws + zn * s * hd;
+  float* dkacc = D + zn * s;
+  float* dvacc = dkacc + zn * s * hd;
+  const int nq = (s + 127) / 128;
+  const BwdWork* work = bwd_work((int)zn, nq, st);
   MP_CUDA(cudaMemsetAsync(dqacc, 0, sizeof(float) * zn * s * hd, st));
+  if (work) MP_CUDA(cudaMemsetAsync(dkacc, 0, sizeof(float) * 2 * zn * s * hd, st));
   {
     const long long rows = zn * s;
     flash_bwd_dot_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(dO),
@@ -677,6 +807,9 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   a.scale_log2 = 1.4426950408889634f * a.scale;
   a.dp = dp;
   a.trace = nullptr;
+  a.work = work ? work->dev : nullptr;
+  a.dKacc = dkacc;
+  a.dVacc = dvacc;
   {
     static long long* dtrace = nullptr;
     if (getenv("MP_FA_TRACE")) {
@@ -694,18 +827,114 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
     if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  if (dp.on()) flash_bwd_kernel<true><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
-  else flash_bwd_kernel<false><<<(unsigned)(zn * a.nq), fa::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
+  const unsigned grid = work ? (unsigned)work->n : (unsigned)(zn * a.nq);
+  if (dp.on()) flash_bwd_kernel<true><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
+  else flash_bwd_kernel<false><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
   count_launch();
   {
     const long long n = zn * s * hd / 2;
-    flash_bwd_dq_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(dqacc, reinterpret_cast<__nv_bfloat16*>(dQKV), s,
-                                                                    (int)zn, hd, ldq);
-    count_launch();
+    if (work) {   // dQ, dK, dV (dK / dV accumulators are contiguous after D)
+      flash_bwd_dq_kernel<<<dim3((unsigned)((n + 255) / 256), 1), 256, 0, st>>>(
+          dqacc, reinterpret_cast<__nv_bfloat16*>(dQKV), s, (int)zn, hd, ldq, 0, 0);
+      flash_bwd_dq_kernel<<<dim3((unsigned)((n + 255) / 256), 2), 256, 0, st>>>(
+          dkacc, reinterpret_cast<__nv_bfloat16*>(dQKV), s, (int)zn, hd, ldq, 1, zn * s * hd);
+      count_launch(2);
+    } else {
+      flash_bwd_dq_kernel<<<dim3((unsigned)((n + 255) / 256), 1), 256, 0, st>>>(
+          dqacc, reinterpret_cast<__nv_bfloat16*>(dQKV), s, (int)zn, hd, ldq, 0, 0);
+      count_launch();
+    }
   }
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd launch: %s", cudaGetErrorString(e));
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa_attr{};
+    cudaFuncGetAttributes(&fa_attr, flash_bwd_kernel<false>);
+    return set_err(MP_ECUDA, "flash attention bwd launch: %s (kernel: %d regs, max %d threads, %zu local B)",
+                   cudaGetErrorString(e), fa_attr.numRegs, fa_attr.maxThreadsPerBlock, fa_attr.localSizeBytes);
+  }
   return MP_OK;
+}
+
+// Split-KV combine: per (z, query tile) and row, merge the partial results
+// (O_p, m_p, l_p) of its nsplit CTAs: M = max m_p, l = sum l_p 2^(m_p - M),
+// O = sum O_p 2^(m_p - M) / l, L2 = M + log2 l.  first[zq] = first slot, the
+// slots of one tile are consecutive.
+__global__ void flash_fwd_combine_kernel(const float* __restrict__ Opart, const float2* __restrict__ ml,
+                                         const int2* __restrict__ tiles, __nv_bfloat16* __restrict__ O, float* L2,
+                                         int s, int nq, int hd, long long ldo) {
+  // block (tile zq, 4-column chunk c4), thread = row: all loads independent across threads
+  const int zq = blockIdx.x, c4 = blockIdx.y, r = threadIdx.x;
+  const int z = zq / nq, qt = zq % nq;
+  const int q = qt * 128 + r;
+  if (q >= s) return;
+  const int2 t = tiles[zq];               // (first slot, count <= 16)
+  float2 v[16];
+  float M = -FLT_MAX;
+#pragma unroll
+  for (int p = 0; p < 16; ++p)
+    if (p < t.y) { v[p] = ml[(long long)(t.x + p) * 128 + r]; M = fmaxf(M, v[p].x); }
+  float l = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int p = 0; p < 16; ++p)
+    if (p < t.y) {
+      const float w = ex2f(v[p].x - M);
+      l += v[p].y * w;
+      const float4 o = reinterpret_cast<const float4*>(Opart)[((long long)(t.x + p) * (hd / 4) + c4) * 128 + r];
+      acc.x += o.x * w; acc.y += o.y * w; acc.z += o.z * w; acc.w += o.w * w;
+    }
+  const float inv = 1.f / l;
+  __nv_bfloat16* orow = O + (long long)q * ldo + (long long)z * hd + 4 * c4;
+  *reinterpret_cast<__nv_bfloat162*>(orow) = __floats2bfloat162_rn(acc.x * inv, acc.y * inv);
+  *reinterpret_cast<__nv_bfloat162*>(orow + 2) = __floats2bfloat162_rn(acc.z * inv, acc.w * inv);
+  if (c4 == 0) L2[(long long)z * s + q] = M + log2f(l);
+}
+
+// Split-KV decomposition of the forward for small b * heads (cf. bwd_work):
+// a query tile's causal kv range [0, qt] is cut into <= 16 chunks of L tiles.
+struct FwdWork { int4* dev = nullptr; int2* tiles = nullptr; int n = 0; float* Opart = nullptr; float2* ml = nullptr; };
+static const FwdWork* fwd_work(int zn, int nq, int hd) {
+  static std::map<std::tuple<int, int, int>, FwdWork> cache;
+  auto key = std::make_tuple(zn, nq, hd);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second.dev ? &it->second : nullptr;
+  const int M = num_sms();
+  auto jobs_for = [&](int L) {
+    std::vector<double> j;
+    for (int z = 0; z < zn; ++z)
+      for (int qt = 0; qt < nq; ++qt)
+        for (int c = 0; c <= qt; c += L) j.push_back(std::min(L, qt + 1 - c) + 1.0 + (L < nq ? 0.5 : 0.0));
+    return j;
+  };
+  int bestL = nq;
+  double best = makespan(jobs_for(nq), M);
+  for (int L : {8, 6, 5, 4, 3, 2}) {
+    if (L >= nq || (nq + L - 1) / L > 16) continue;
+    const double m = makespan(jobs_for(L), M) + 3.0;   // + the combine pass
+    if (m < 0.85 * best) { best = m; bestL = L; }
+  }
+  if (const char* e = getenv("MP_FA_FWD_SPLIT_L")) bestL = std::max(1, std::min(nq, atoi(e)));   // tuning sweeps
+  FwdWork w;
+  if (bestL < nq) {
+    std::vector<int4> items;
+    std::vector<int2> tiles;
+    for (int z = 0; z < zn; ++z)
+      for (int qt = 0; qt < nq; ++qt) {
+        tiles.push_back(make_int2((int)items.size(), (qt + bestL) / bestL));
+        for (int c = 0; c <= qt; c += bestL)
+          items.push_back(make_int4((z << 16) | qt, c, std::min(qt + 1, c + bestL), (int)items.size()));
+      }
+    std::stable_sort(items.begin(), items.end(), [](const int4& a, const int4& b) { return a.z - a.y > b.z - b.y; });
+    bool ok = cudaMalloc(&w.dev, items.size() * sizeof(int4)) == cudaSuccess &&
+              cudaMalloc(&w.tiles, tiles.size() * sizeof(int2)) == cudaSuccess &&
+              cudaMalloc(&w.Opart, items.size() * 128 * (size_t)hd * sizeof(float)) == cudaSuccess &&
+              cudaMalloc(&w.ml, items.size() * 128 * sizeof(float2)) == cudaSuccess &&
+              cudaMemcpy(w.dev, items.data(), items.size() * sizeof(int4), cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(w.tiles, tiles.data(), tiles.size() * sizeof(int2), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok) w.n = (int)items.size(); else w.dev = nullptr;
+  }
+  auto& ref = cache[key] = w;
+  return ref.dev ? &ref : nullptr;
 }
 
 // QKV: [s, b, heads, 3, hd] bf16; O: [s, b, heads, hd] bf16; L2: [b*heads, s] fp32.
@@ -750,11 +979,20 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
     if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
-  const long long grid = z * a.nq;
+  const FwdWork* work = (z < 65536 && a.nq < 65536) ? fwd_work((int)z, a.nq, hd) : nullptr;
+  a.work = work ? work->dev : nullptr;
+  a.Opart = work ? work->Opart : nullptr;
+  a.ml = work ? work->ml : nullptr;
+  const long long grid = work ? work->n : z * a.nq;
   if (grid > 0x7fffffffLL) return set_err(MP_EINVAL, "flash attention: grid too large");
   if (dp.on()) flash_fwd_kernel<true><<<(unsigned)grid, fa::THREADS, fa::SMEM, st>>>(tq, tk, tv, a);
   else flash_fwd_kernel<false><<<(unsigned)grid, fa::THREADS, fa::SMEM, st>>>(tq, tk, tv, a);
   count_launch();
+  if (work) {
+    flash_fwd_combine_kernel<<<dim3((unsigned)(z * a.nq), (unsigned)(hd / 4)), 128, 0, st>>>(
+        work->Opart, work->ml, work->tiles, a.O, L2, s, a.nq, hd, a.ldo);
+    count_launch();
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention launch: %s", cudaGetErrorString(e));
   return MP_OK;
@@ -765,7 +1003,7 @@ long long* g_fa_trace = nullptr;
 }  // namespace mp
 
 extern "C" long long mp_op_flash_attn_bwd_ws_floats(int s, int b, int heads, int hd) {
-  return (long long)b * heads * s * (hd + 1);
+  return mp::flash_bwd_ws_floats(s, b, heads, hd);
 }
 
 extern "C" mp_status mp_op_flash_attn_bwd(const void* qkv, const void* ctx, const void* dctx, const float* lse2,

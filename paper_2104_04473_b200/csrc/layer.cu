@@ -29,6 +29,7 @@ namespace mp {
 mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st);
 mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st,
                          Dropout dp);
+long long flash_bwd_ws_floats(int s, int b, int heads, int hd);
 mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const float* L2, void* dQKV, float* ws,
                          int s, int b, int heads, int hd, cudaStream_t st, Dropout dp);
 
@@ -136,7 +137,7 @@ mp_status ensure_workspace(mp_ctx* c, int b) {
                     (size_t)d.T * d.ht * es};
   for (int i = 0; i < 7; ++i) MP_CUDA(cudaMalloc(bufs[i], al256(sizes[i])));
   MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * std::max(1LL, mp_op_layernorm_bwd_scratch_floats(d.T, d.h)))));
-  if (fused) MP_CUDA(cudaMalloc(&c->ws_fa, al256(sizeof(float) * (size_t)d.z * d.s * (d.hd + 1))));
+  if (fused) MP_CUDA(cudaMalloc(&c->ws_fa, al256(sizeof(float) * (size_t)flash_bwd_ws_floats(d.s, d.b, d.heads, d.hd))));
   c->ws_b = b;
   return MP_OK;
 }
