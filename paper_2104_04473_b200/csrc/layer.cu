@@ -258,10 +258,15 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
     MP_TRY(flash_attn_fwd(st.QKV, st.ctx, (float*)st.P, d.s, d.b, d.heads, d.hd, c->cs, dpa));
   else
     MP_TRY(attention_fwd<T>(c, d, st.QKV, st.P, st.ctx, dpa));
-  const bool nv = c->tps.on, nvr = nv && !tp_sym_debug_local();
+  const bool nv = c->tps.on, two = nv && tp_sym_two_shot(c), nvr = nv && !two && !tp_sym_debug_local();
   void* zw; const void* zr;   // partial-product buffer: GEMM writes zw, the consumer reads zr
-  // g (a11): NCCL all-reduce in place, or NVLS barrier + reduce-load inside the consumer
-  auto g_op = [&]() -> mp_status { return nv ? tp_sym_barrier(c, c->cs) : allreduce(c, zw, (size_t)d.T * d.h, c->cs); };
+  // g (a11): NCCL all-reduce in place; NVLS one-shot: barrier + reduce-load inside the consumer;
+  // NVLS two-shot: slab reduce-load + multicast store, the consumer reads the local sum
+  auto g_op = [&]() -> mp_status {
+    if (!nv) return allreduce(c, zw, (size_t)d.T * d.h, c->cs);
+    if (two) return tp_sym_reduce_two_shot(c, (size_t)d.T * d.h, c->cs, &zr);
+    return tp_sym_barrier(c, c->cs);
+  };
   auto z_next = [&]() {
     if (nv) tp_sym_next(c, &zw, &zr); else { zw = c->ws_z; zr = c->ws_z; }
     if (nv && !nvr) zr = zw;
@@ -312,7 +317,7 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]), d.T, d.h4t, c->cs));
   // f (a17): NVLS -- dgrad writes its partial into the symmetric buffer, dW1 accumulates, one barrier,
   // and the LayerNorm backward reduce-loads the sum; NCCL -- all-reduce dA2 on the side stream during dW1
-  const bool nv = c->tps.on, nvr = nv && !tp_sym_debug_local();
+  const bool nv = c->tps.on, two = nv && tp_sym_two_shot(c), nvr = nv && !two && !tp_sym_debug_local();
   void* fw = dA2; const void* fr = dA2;
   if (nv) tp_sym_next(c, &fw, &fr);
   if (nv && !nvr) fr = fw;
@@ -332,7 +337,8 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
     MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h, c->side));
     gemm_set_max_ctas(0);
     MP_CUDA(cudaEventRecord(ev_b, c->side));
-    MP_TRY(tp_sym_barrier(c, c->cs));
+    if (two) MP_TRY(tp_sym_reduce_two_shot(c, (size_t)d.T * d.h, c->cs, &fr));
+    else MP_TRY(tp_sym_barrier(c, c->cs));
   } else {
     MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
   }
@@ -375,7 +381,8 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
     MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h, c->side));
     gemm_set_max_ctas(0);
     MP_CUDA(cudaEventRecord(ev_b, c->side));
-    MP_TRY(tp_sym_barrier(c, c->cs));
+    if (two) MP_TRY(tp_sym_reduce_two_shot(c, (size_t)d.T * d.h, c->cs, &fr));
+    else MP_TRY(tp_sym_barrier(c, c->cs));
   } else {
     MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
   }

@@ -7,6 +7,7 @@
 
 #include <cstdlib>
 #include <string>
+#include <algorithm>
 
 #include "common.h"
 #include "runtime.h"
@@ -67,7 +68,7 @@ mp_status tp_sym_ensure(mp_ctx* c, size_t buf_bytes) {
   tp_sym_free(c);
   s.tried = true;
   buf_bytes = (buf_bytes + 4095) & ~size_t(4095);
-  const size_t total = FLAG_BYTES + 2 * buf_bytes;
+  const size_t total = FLAG_BYTES + 4 * buf_bytes;   // 2 partial-sum buffers + 2 landing buffers
   int mc_ok = 0;
   {
     using attr_fn = CUresult (*)(int*, CUdevice_attribute, CUdevice);
@@ -155,6 +156,59 @@ void tp_sym_next(mp_ctx* c, void** local, const void** mc) {
   const size_t off = FLAG_BYTES + (size_t)(s.next++ & 1) * s.buf_bytes;
   *local = reinterpret_cast<char*>(s.base) + off;
   *mc = s.mc + off;
+}
+
+bool tp_sym_two_shot(const mp_ctx* c) {
+  static const int shot = getenv("MP_TP_NVLS_SHOT") ? atoi(getenv("MP_TP_NVLS_SHOT")) : 0;
+  if (shot == 1) return false;
+  if (shot == 2) return true;
+  return c->t >= 4;
+}
+
+// slab [v0, v1) of 16-byte vectors: sum over the TP group (NVSwitch reduce-load,
+// fp32 accumulation) multicast-stored to every rank's landing buffer
+template <bool BF16>
+__global__ void tp_rs_ag_kernel(const char* __restrict__ part_mc, char* __restrict__ land_mc, long long v0,
+                                long long v1) {
+  for (long long i = v0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < v1;
+       i += (long long)gridDim.x * blockDim.x) {
+    const char* src = part_mc + 16 * i;
+    char* dst = land_mc + 16 * i;
+    uint32_t a, b, cc, d;
+    if constexpr (BF16) {
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a), "=r"(b), "=r"(cc), "=r"(d) : "l"(src) : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.v4.bf16x2 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(a), "r"(b),
+                   "r"(cc), "r"(d) : "memory");
+    } else {
+      asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=r"(a), "=r"(b), "=r"(cc), "=r"(d) : "l"(src) : "memory");
+      asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "r"(a), "r"(b),
+                   "r"(cc), "r"(d) : "memory");
+    }
+  }
+  __threadfence_system();   // stores performed before the following barrier's release
+}
+
+mp_status tp_sym_reduce_two_shot(mp_ctx* c, size_t n_elems, cudaStream_t st, const void** out) {
+  TpSym& s = c->tps;
+  const size_t slot = (size_t)((s.next - 1) & 1);
+  const size_t poff = FLAG_BYTES + slot * s.buf_bytes, loff = FLAG_BYTES + (2 + slot) * s.buf_bytes;
+  const long long nvec = (long long)(n_elems * c->esz / 16);
+  const long long v0 = nvec * c->tp / c->t, v1 = nvec * (c->tp + 1) / c->t;
+  MP_TRY(tp_sym_barrier(c, st));                      // all partial sums written
+  const long long n = v1 - v0;
+  const int grid = (int)std::max(1LL, std::min<long long>((n + 255) / 256, 4LL * num_sms()));
+  if (c->cfg.dtype == MP_BF16)
+    tp_rs_ag_kernel<true><<<grid, 256, 0, st>>>(s.mc + poff, s.mc + loff, v0, v1);
+  else
+    tp_rs_ag_kernel<false><<<grid, 256, 0, st>>>(s.mc + poff, s.mc + loff, v0, v1);
+  count_launch();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_err(MP_ECUDA, "tp two-shot: %s", cudaGetErrorString(e));
+  MP_TRY(tp_sym_barrier(c, st));                      // every slab stored on every rank
+  *out = reinterpret_cast<char*>(s.base) + loff;
+  return MP_OK;
 }
 
 bool tp_sym_debug_local() { return debug_mode() == 1; }

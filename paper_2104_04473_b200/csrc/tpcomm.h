@@ -36,6 +36,14 @@ struct TpSym {
 mp_status tp_sym_ensure(mp_ctx* c, size_t buf_bytes);
 // Next buffer: local pointer for the producer, multicast pointer for the consumer.
 void tp_sym_next(mp_ctx* c, void** local, const void** mc);
+// Two-shot variant (t >= 4 by default; MP_TP_NVLS_SHOT=1|2 overrides): after
+// the barrier, every rank reduce-loads only its 1/t slab of the partial sums
+// and multicast-stores the sum into the landing buffer paired with the last
+// buffer handed out; after a second barrier every rank holds the full sum in
+// its local copy (returned in *out).  NVLink egress per GPU ~ (1 + 1/t) x the
+// tensor instead of t x (one-shot).
+bool tp_sym_two_shot(const mp_ctx* c);
+mp_status tp_sym_reduce_two_shot(mp_ctx* c, size_t n_elems, cudaStream_t st, const void** out);
 // All TP ranks' partials written (every prior kernel of this stream on every rank done).
 mp_status tp_sym_barrier(mp_ctx* c, cudaStream_t st);
 void tp_sym_free(mp_ctx* c);

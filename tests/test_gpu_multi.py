@@ -119,3 +119,25 @@ def test_multi_gpu_tp_transport(tmp_path, t, p, v, m, sched, tpcomm, dtype):
     assert r.returncode == 0, msg
     assert len(reps) == n and all(x["ok"] for x in reps), msg
     assert all(x.get("tp_comm") == tpcomm for x in reps), msg
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("t,shot", [(2, "2"), (4, "1")])
+def test_multi_gpu_nvls_shot_variants(tmp_path, t, shot, dtype):
+    """NVLS one-shot (reduce-load fused into the consumer) and two-shot (slab
+    reduce-load + multicast store) give the oracle's results at either t
+    (the default picks one-shot at t = 2, two-shot at t >= 4)."""
+    if ngpus() < t:
+        pytest.skip(f"needs {t} GPUs")
+    out = str(tmp_path / "rep")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={t}",
+           "--master-addr=127.0.0.1", f"--master-port={37000 + (hash((t, shot, dtype)) % 2000)}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    env = dict(os.environ, MP_TP_NVLS_SHOT=shot,
+               MP_WORKER_ARGS=f"--tp {t} --pp 1 --vp 1 --m 4 --sched 1f1b --dtype {dtype} --tpcomm nvls --out {out}")
+    env.pop("MP_TP_COMM", None)
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
+    msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
+    assert r.returncode == 0, msg
+    assert len(reps) == t and all(x["ok"] for x in reps), msg
