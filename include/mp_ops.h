@@ -37,6 +37,9 @@ extern "C" {
  *   2 reduction limited to k < min(K, 128*(floor(m/128)+1)): P V and dS K,
  *     whose A operand is zero above the diagonal;
  *   3 reduction limited to k >= 128*floor(m/128): P^T dO and dS^T Q.
+ * act = 1 (bf16 only; the fused bias-GeLU of a15): C = x, C2 = gelu(x)
+ *   with x = alpha A B + bias in fp32, both bf16 [M, N] with ldc / strideC
+ *   (tanh form of GeLU, as in the oracle); act = 0: C2 unused.
  * bf16 runs on the tcgen05 tensor cores (TMA-fed, TMEM accumulators);
  * fp32 runs a SIMT FFMA kernel (tcgen05 has no fp32 kind). */
 typedef struct {
@@ -50,6 +53,8 @@ typedef struct {
   int accumulate;
   int causal;
   float alpha;
+  int act;
+  void* C2;
 } mp_gemm_desc;
 
 mp_status mp_op_gemm(mp_dtype dtype, const mp_gemm_desc* g, void* stream);

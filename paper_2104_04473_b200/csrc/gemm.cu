@@ -58,6 +58,8 @@ struct TcArgs {
   int c_fp32, accumulate, causal, vec_ok;
   int tma_out;          // epilogue through shared memory + TMA store / reduce-add (tmC valid)
   int stream_k;         // accumulate mode: CTAs split the (tile, k-block) iterations evenly
+  int n_fast;           // tile order n-block fastest (consecutive tiles share the A panel)
+  int act;              // 1: bf16 C = x and C2 = gelu(x) (tmC2 valid)
   int kb_per_tile;      // k-blocks per tile (stream_k)
   float alpha;
 };
@@ -71,6 +73,14 @@ __device__ __forceinline__ void k_range(const TcArgs& g, int m_blk, int& kb0, in
   if (g.causal == 2) kend = min(g.K, (m_blk + 1) * BM);
   if (g.causal == 3) kb0 = (m_blk * BM) / BK;
   kb1 = (kend + BK - 1) / BK;
+}
+
+// GeLU, tanh form (P:146 / oracle.layer.gelu), tanh on the SFU (tanh.approx:
+// |rel err| ~ 2^-11, below the bf16 rounding of the stored result)
+__device__ __forceinline__ float gelu_fast(float u) {
+  float th;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(0.7978845608028654f * (u + 0.044715f * u * u * u)));
+  return 0.5f * u * (1.f + th);
 }
 
 // Work sequence of one CTA, identical for the producer, MMA and epilogue roles.
@@ -107,7 +117,8 @@ struct WorkIter {
       tile = t;
       t += gridDim.x;
       const int rem = tile % tiles_per_batch;
-      const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+      const int n_blk = g.n_fast ? rem % g.n_blocks : rem / g.m_blocks;
+      const int m_blk = g.n_fast ? rem / g.n_blocks : rem % g.m_blocks;
       if (tile_skipped(g, m_blk, n_blk, BN)) continue;
       k_range(g, m_blk, kb0, kb1);
       return true;
@@ -119,7 +130,7 @@ struct WorkIter {
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmC, TcArgs g) {
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, TcArgs g) {
   using Cfg = TcCfg<BN>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -145,6 +156,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (g.tma_out) tma_prefetch(&tmC);
+    if (g.act) tma_prefetch(&tmC2);
   }
   if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   tc_fence_before();
@@ -161,7 +173,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int t, kb0, kb1;
       while (it.next<BN>(g, t, kb0, kb1)) {
         const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
-        const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+        const int n_blk = g.n_fast ? rem % g.n_blocks : rem / g.m_blocks;
+      const int m_blk = g.n_fast ? rem / g.n_blocks : rem % g.m_blocks;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
@@ -231,7 +244,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int t, kb0, kb1;
     while (it.next<BN>(g, t, kb0, kb1)) {
       const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
-      const int n_blk = rem / g.m_blocks, m_blk = rem % g.m_blocks;
+      const int n_blk = g.n_fast ? rem % g.n_blocks : rem / g.m_blocks;
+      const int m_blk = g.n_fast ? rem / g.n_blocks : rem % g.m_blocks;
       const bool have_acc = kb1 > kb0;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
@@ -266,28 +280,43 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                            __float_as_uint(v[2]), __float_as_uint(v[3]));
             }
           } else {
+            float x[64];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
               uint32_t r[32];
               tmem_ld_32x32b_x32(tbase + c0 + 32 * hf, r);
               tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
+              for (int c = 0; c < 32; ++c) {
+                float a0 = have_acc ? __uint_as_float(r[c]) * g.alpha : 0.f;
+                const int gc = col0 + 32 * hf + c;
+                if (g.bias && gc < g.N) a0 += __bfloat162float(g.bias[gc]);
+                x[32 * hf + c] = a0;
+              }
+            }
+            // pass 0: x (the output, or the pre-activation when act); pass 1 (act): gelu(x)
+            for (int pass = 0; pass < (g.act ? 2 : 1); ++pass) {
+              if (pass == 1) {
+                // the pre-activation box goes out first, then GeLU reuses the staging buffer
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                  tma_store_3d(&tmC, buf, col0, row0, z);
+                  bulk_commit();
+                  bulk_wait_read<0>();
+                }
+                __syncwarp();
+#pragma unroll
+                for (int e = 0; e < 64; ++e) x[e] = gelu_fast(x[e]);
+              }
+#pragma unroll
+              for (int chunk = 0; chunk < 8; ++chunk) {
                 uint32_t w[4];
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                  const int c = 8 * j + 2 * e;
-                  float a0 = have_acc ? __uint_as_float(r[c]) * g.alpha : 0.f;
-                  float a1 = have_acc ? __uint_as_float(r[c + 1]) * g.alpha : 0.f;
-                  const int gc = col0 + 32 * hf + c;
-                  if (g.bias) {
-                    if (gc < g.N) a0 += __bfloat162float(g.bias[gc]);
-                    if (gc + 1 < g.N) a1 += __bfloat162float(g.bias[gc + 1]);
-                  }
-                  __nv_bfloat162 pr = __floats2bfloat162_rn(a0, a1);
+                  __nv_bfloat162 pr = __floats2bfloat162_rn(x[8 * chunk + 2 * e], x[8 * chunk + 2 * e + 1]);
                   w[e] = *reinterpret_cast<uint32_t*>(&pr);
                 }
-                const int chunk = 4 * hf + j;
                 st_shared_v4(rowaddr + ((chunk ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
               }
             }
@@ -296,7 +325,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           __syncwarp();
           if (lane == 0) {
             if (g.accumulate) tma_reduce_add_3d(&tmC, buf, col0, row0, z);
-            else tma_store_3d(&tmC, buf, col0, row0, z);
+            else tma_store_3d(g.act ? &tmC2 : &tmC, buf, col0, row0, z);
             bulk_commit();
           }
         }
@@ -445,8 +474,8 @@ static int pick_bn(const mp_gemm_desc& g) {
 }
 
 template <int BN, bool A_MN, bool B_MN>
-static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const TcArgs& a,
-                             int grid, cudaStream_t st) {
+static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                             const CUtensorMap& tc2, const TcArgs& a, int grid, cudaStream_t st) {
   using Cfg = TcCfg<BN>;
   auto k = tc_gemm_kernel<BN, A_MN, B_MN>;
   static bool attr = false;
@@ -455,17 +484,17 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, a);
+  k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tc2, a);
   return cudaGetLastError();
 }
 
 template <int BN>
 static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
-                                  const TcArgs& a, int grid, int am, int bm, cudaStream_t st) {
-  if (!am && !bm) return launch_tc<BN, false, false>(ta, tb, tc, a, grid, st);
-  if (!am && bm) return launch_tc<BN, false, true>(ta, tb, tc, a, grid, st);
-  if (am && !bm) return launch_tc<BN, true, false>(ta, tb, tc, a, grid, st);
-  return launch_tc<BN, true, true>(ta, tb, tc, a, grid, st);
+                                  const CUtensorMap& tc2, const TcArgs& a, int grid, int am, int bm, cudaStream_t st) {
+  if (!am && !bm) return launch_tc<BN, false, false>(ta, tb, tc, tc2, a, grid, st);
+  if (!am && bm) return launch_tc<BN, false, true>(ta, tb, tc, tc2, a, grid, st);
+  if (am && !bm) return launch_tc<BN, true, false>(ta, tb, tc, tc2, a, grid, st);
+  return launch_tc<BN, true, true>(ta, tb, tc, tc2, a, grid, st);
 }
 
 // CTA budget of the next persistent GEMM launches (0 = every SM): lets a GEMM
@@ -517,21 +546,38 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   memset(&tc, 0, sizeof(tc));
   // epilogue via TMA: C box = 32 rows x 128 bytes
   a.tma_out = a.vec_ok && make_map(&tc, g.C, g.N, g.M, g.batch, g.ldc, g.strideC, 32, esz);
+  CUtensorMap tc2;
+  memset(&tc2, 0, sizeof(tc2));
+  a.act = g.act;
+  if (g.act) {
+    if (g.c_fp32 || g.accumulate || !a.tma_out || !al16(g.C2) ||
+        !make_map(&tc2, g.C2, g.N, g.M, g.batch, g.ldc, g.strideC, 32, esz))
+      return set_err(MP_EINVAL, "gemm: act needs bf16 C / C2, 16-byte aligned, no accumulate");
+  }
   a.kb_per_tile = (g.K + BK - 1) / BK;
+  // Raster: by default consecutive tiles share the B panel (m fastest).  When A
+  // is the large operand and B fits comfortably in L2 (e.g. the logit-layer
+  // weight gradient dE = dlogits^T Z, A = 210 MB, B = 9 MB), walk n fastest so
+  // every A panel is streamed from DRAM once instead of once per n-block.
+  {
+    const double a_bytes = 2.0 * g.M * (double)g.K * g.batch, b_bytes = 2.0 * g.N * (double)g.K * g.batch;
+    a.n_fast = (a.n_blocks > 1 && a_bytes > 2.0 * b_bytes && b_bytes < 32e6) ? 1 : 0;
+  }
   a.stream_k = 0;
   static const bool no_sk = getenv("MP_GEMM_NO_STREAMK") != nullptr;
   a.stream_k = want_stream_k(a) && !no_sk;
   const int grid = tc_grid(a);
   cudaError_t e;
-  if (BN == 64) e = dispatch_major<64>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);
-  else if (BN == 128) e = dispatch_major<128>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);
-  else e = dispatch_major<256>(ta, tb, tc, a, grid, g.a_major, g.b_major, st);
+  if (BN == 64) e = dispatch_major<64>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+  else if (BN == 128) e = dispatch_major<128>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+  else e = dispatch_major<256>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
   if (e != cudaSuccess) return set_err(MP_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
   return MP_OK;
 }
 
 mp_status gemm_fp32(const mp_gemm_desc& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return set_err(MP_EINVAL, "gemm: empty shape");
+  if (g.act) return set_err(MP_EUNSUPPORTED, "gemm: the fused GeLU epilogue is bf16-only");
   dim3 grid((g.M + SB_M - 1) / SB_M, (g.N + SB_N - 1) / SB_N, g.batch);
   simt_gemm_kernel<<<grid, 256, 0, st>>>(g, grid.x, grid.y);
   cudaError_t e = cudaGetLastError();

@@ -48,7 +48,7 @@ mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, 
 // H = gelu(Y + b)
 template <class T>
 mp_status bias_gelu_fwd(const T* yv, const T* b, T* out, long long R, int N, cudaStream_t st);
-// dU = dH * gelu'(Y + b) (written to du), db += colsum(dU)
+// dU = dH * gelu'(Y + b) (written to du), db += colsum(dU); b may be null (Y already biased)
 template <class T>
 mp_status bias_gelu_bwd(const T* dh, const T* yv, const T* b, T* du, float* db, int R, int N, cudaStream_t st);
 // out[n] += sum_r X[r, n]

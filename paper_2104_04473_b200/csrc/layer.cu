@@ -66,6 +66,16 @@ static mp_status lin_fwd(mp_ctx* c, const void* X, const void* W, const void* bi
   g.c_fp32 = c->cfg.dtype == MP_FP32;
   return gemm(c->cfg.dtype, g, c->cs);
 }
+// bf16: U = X W^T + bias and H = gelu(U) from one GEMM epilogue (a14 + a15 fused)
+static mp_status lin_fwd_gelu(mp_ctx* c, const void* X, const void* W, const void* bias, void* U, void* H, int T,
+                              int N, int K) {
+  mp_gemm_desc g{};
+  g.M = T; g.N = N; g.K = K; g.batch = 1;
+  g.A = X; g.lda = K; g.B = W; g.ldb = K; g.C = U; g.ldc = N;
+  g.bias = bias; g.alpha = 1.f;
+  g.act = 1; g.C2 = H;
+  return gemm(c->cfg.dtype, g, c->cs);
+}
 // dX[T, K] = dY[T, N] W[N, K]
 static mp_status lin_dgrad(mp_ctx* c, const void* dY, const void* W, void* dX, int T, int N, int K) {
   mp_gemm_desc g{};
@@ -106,6 +116,12 @@ static Dims dims(mp_ctx* c, int b) {
   d.heads = c->cfg.a / c->t; d.hd = d.h / c->cfg.a;
   d.z = (long long)b * d.heads; d.sq = (long long)d.s * d.s;
   return d;
+}
+
+// FC1 bias + GeLU in the GEMM epilogue (bf16 path)?
+static bool fuse_gelu(const mp_ctx* c) {
+  static const bool off = getenv("MP_NO_GELU_EPILOGUE") != nullptr;   // ablation
+  return c->cfg.dtype == MP_BF16 && !off;
 }
 
 // fused tcgen05 attention core usable for this configuration?
@@ -276,8 +292,12 @@ static mp_status layer_fwd_t(mp_ctx* c, int layer, int b, const void* x, void* y
   MP_TRY(g_op());
   MP_TRY(bda_layernorm_fwd<T>((const T*)zr, ptr<T>(c, lp[P_BO]), X, (T*)st.X1, ptr<T>(c, lp[P_LN2G]),
                               ptr<T>(c, lp[P_LN2B]), (T*)st.A2, st.mu2, st.rs2, d.T, d.h, eps, c->cs, dp1, nvr));
-  MP_TRY(lin_fwd(c, st.A2, ptr<T>(c, lp[P_W1]), nullptr, st.Y1, d.T, d.h4t, d.h));
-  MP_TRY(bias_gelu_fwd<T>((const T*)st.Y1, ptr<T>(c, lp[P_B1]), (T*)st.H, d.T, d.h4t, c->cs));
+  if (fuse_gelu(c)) {      // Y1 holds the biased pre-activation
+    MP_TRY(lin_fwd_gelu(c, st.A2, ptr<T>(c, lp[P_W1]), ptr<T>(c, lp[P_B1]), st.Y1, st.H, d.T, d.h4t, d.h));
+  } else {
+    MP_TRY(lin_fwd(c, st.A2, ptr<T>(c, lp[P_W1]), nullptr, st.Y1, d.T, d.h4t, d.h));
+    MP_TRY(bias_gelu_fwd<T>((const T*)st.Y1, ptr<T>(c, lp[P_B1]), (T*)st.H, d.T, d.h4t, c->cs));
+  }
   z_next();
   MP_TRY(lin_fwd(c, st.H, ptr<T>(c, lp[P_W2]), nullptr, zw, d.T, d.h, d.h4t));
   MP_TRY(g_op());
@@ -314,7 +334,8 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   }
   MP_TRY(lin_dgrad(c, dZ2, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
   MP_TRY(lin_wgrad(c, dZ2, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
-  MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]), d.T, d.h4t, c->cs));
+  MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, fuse_gelu(c) ? nullptr : ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]),
+                          d.T, d.h4t, c->cs));
   // f (a17): NVLS -- dgrad writes its partial into the symmetric buffer, dW1 accumulates, one barrier,
   // and the LayerNorm backward reduce-loads the sum; NCCL -- all-reduce dA2 on the side stream during dW1
   const bool nv = c->tps.on, two = nv && tp_sym_two_shot(c), nvr = nv && !two && !tp_sym_debug_local();

@@ -63,7 +63,8 @@ class GemmDesc(ctypes.Structure):
                 ("B", ctypes.c_void_p), ("ldb", ctypes.c_longlong), ("strideB", ctypes.c_longlong),
                 ("C", ctypes.c_void_p), ("ldc", ctypes.c_longlong), ("strideC", ctypes.c_longlong),
                 ("bias", ctypes.c_void_p), ("c_fp32", ctypes.c_int), ("accumulate", ctypes.c_int),
-                ("causal", ctypes.c_int), ("alpha", ctypes.c_float)]
+                ("causal", ctypes.c_int), ("alpha", ctypes.c_float), ("act", ctypes.c_int),
+                ("C2", ctypes.c_void_p)]
 
 
 _lib = None

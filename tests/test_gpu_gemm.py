@@ -151,3 +151,39 @@ def test_gemm_bf16_stream_k_accumulate(am, bm, M, N, K):
     the SMs and partial tiles are reduce-added into the fp32 accumulator."""
     got, ref = run_gemm(M, N, K, 1, am, bm, c_fp32=True, accumulate=True)
     assert normwise(got, ref) < 1e-4
+
+
+@pytest.mark.parametrize("M,N,K", [(2048, 2304, 576), (304, 520, 200), (96, 1000, 136)])
+def test_gemm_bf16_gelu_epilogue(M, N, K):
+    """act = 1: one GEMM writes the biased pre-activation U = A B + bias and
+    H = gelu(U) (the FC1 + bias-GeLU of the MLP block, a14 + a15)."""
+    from oracle.layer import gelu
+    A = gen.activations((1, M, K), 7, 1.0, "bf16")
+    Bt = gen.activations((1, N, K), 8, 1.0, "bf16")
+    bvec = gen.activations((N,), 9, 1.0, "bf16")
+    dA, dB, db = dev(A, "bf16"), dev(Bt, "bf16"), dev(bvec, "bf16")
+    U = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+    H = torch.zeros_like(U)
+    d = mp.GemmDesc()
+    d.M, d.N, d.K, d.batch = M, N, K, 1
+    d.A, d.lda, d.strideA = dA.data_ptr(), K, M * K
+    d.B, d.ldb, d.strideB = dB.data_ptr(), K, N * K
+    d.C, d.ldc, d.strideC = U.data_ptr(), N, M * N
+    d.bias = db.data_ptr()
+    d.alpha = 1.0
+    d.act = 1
+    d.C2 = H.data_ptr()
+    mp.mp_op_gemm("bf16", d)
+    torch.cuda.synchronize()
+    ref_u = gemm_ref(A, np.swapaxes(Bt, 1, 2), 1.0, bvec)[0]
+    assert normwise(host(U), ref_u) < 1e-2
+    assert normwise(host(H), gelu(ref_u)) < 1e-2
+
+
+def test_gemm_gelu_epilogue_rejects_fp32():
+    d = mp.GemmDesc()
+    d.M = d.N = d.K = 64
+    d.batch = 1
+    d.act = 1
+    with pytest.raises(mp.MPError):
+        mp.mp_op_gemm("fp32", d)
