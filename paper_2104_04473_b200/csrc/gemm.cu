@@ -37,11 +37,13 @@ constexpr int BK = 64;              // 64 bf16 = 128 B = one swizzle row
 constexpr int EPI_WARPS = 8;               // two warps per TMEM lane quarter
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 
-template <int BN>
+// PAIR: CTA pair (cta_group::2) tile of 256 x BN; each CTA holds 128 rows of A
+// and BN/2 rows of B per stage and accumulates its 128 x BN half in its TMEM.
+template <int BN, bool PAIR = false>
 struct TcCfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = PAIR ? (BN == 256 ? 6 : 8) : (BN == 256 ? 4 : (BN == 128 ? 6 : 8));
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = 2 * BN;
   // epilogue staging: per epilogue warp one 32-row x 128-byte box (TMA store)
@@ -60,6 +62,7 @@ struct TcArgs {
   int stream_k;         // accumulate mode: CTAs split the (tile, k-block) iterations evenly
   int n_fast;           // tile order n-block fastest (consecutive tiles share the A panel)
   int act;              // 1: bf16 C = x and C2 = gelu(x) (tmC2 valid)
+  int pair;             // CTA-pair kernel: m_blocks count 256-row pair tiles
   int kb_per_tile;      // k-blocks per tile (stream_k)
   float alpha;
 };
@@ -92,14 +95,17 @@ __device__ __forceinline__ float gelu_fast(float u) {
 // reduce-added twice.
 struct WorkIter {
   long long i, i1;
-  int t;
+  int t, nb;
   __device__ __forceinline__ explicit WorkIter(const TcArgs& g) {
+    // CTA pairs walk the tiles together: logical block = cluster index
+    const int b = g.pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    nb = g.pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     if (g.stream_k) {
       const long long I = (long long)g.num_tiles * g.kb_per_tile;
-      i = I * blockIdx.x / gridDim.x;
-      i1 = I * (blockIdx.x + 1) / gridDim.x;
+      i = I * b / nb;
+      i1 = I * (b + 1) / nb;
     }
-    t = blockIdx.x;
+    t = b;
   }
   template <int BN>
   __device__ __forceinline__ bool next(const TcArgs& g, int& tile, int& kb0, int& kb1) {
@@ -115,7 +121,7 @@ struct WorkIter {
     const int tiles_per_batch = g.m_blocks * g.n_blocks;
     while (t < g.num_tiles) {
       tile = t;
-      t += gridDim.x;
+      t += nb;
       const int rem = tile % tiles_per_batch;
       const int n_blk = g.n_fast ? rem % g.n_blocks : rem / g.m_blocks;
       const int m_blk = g.n_fast ? rem / g.n_blocks : rem % g.m_blocks;
@@ -127,12 +133,13 @@ struct WorkIter {
   }
 };
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool PAIR>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, TcArgs g) {
-  using Cfg = TcCfg<BN>;
+  using Cfg = TcCfg<BN, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
+  constexpr int TM = PAIR ? 2 * BM : BM;           // rows of one (pair) tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
@@ -146,10 +153,14 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
   const int warp = threadIdx.x / 32;
   const int lane = threadIdx.x % 32;
+  const uint32_t rank = PAIR ? cluster_ctarank() : 0;   // 0 = leader (issues the pair MMAs)
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-    for (int s = 0; s < 2; ++s) { mbar_init(&tfull[s], 1); mbar_init(&tempty[s], EPI_WARPS * 32); }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], (PAIR ? 2 : 1) * EPI_WARPS * 32);   // both CTAs' epilogues release the leader's TMEM
+    }
     fence_mbar_init();
   }
   if (warp == 0 && lane == 0) {
@@ -158,9 +169,13 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (g.tma_out) tma_prefetch(&tmC);
     if (g.act) tma_prefetch(&tmC2);
   }
-  if (warp == 1) tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
+    else tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();      // barriers initialised cluster-wide, TMEM allocated in both CTAs
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int tiles_per_batch = g.m_blocks * g.n_blocks;
@@ -168,40 +183,61 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------ TMA producer
+      // PAIR: both CTAs load their halves (A rows rank*128.., B rows rank*BN/2..)
+      // and signal the leader's full barrier, which the leader arms for both.
+      const uint32_t full_cl0 = PAIR ? mapa_shared(&full[0], 0) : 0;
       int stage = 0; uint32_t phase = 0;
       WorkIter it(g);
       int t, kb0, kb1;
       while (it.next<BN>(g, t, kb0, kb1)) {
         const int z = t / tiles_per_batch, rem = t % tiles_per_batch;
         const int n_blk = g.n_fast ? rem % g.n_blocks : rem / g.m_blocks;
-      const int m_blk = g.n_fast ? rem / g.n_blocks : rem % g.m_blocks;
+        const int m_blk = g.n_fast ? rem / g.n_blocks : rem % g.m_blocks;
+        const int arow = m_blk * TM + (int)rank * BM;
+        const int brow = PAIR ? n_blk * BN + (int)rank * (BN / 2) : n_blk * BN;
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
+          if (rank == 0) mbar_arrive_expect_tx(&full[stage], (PAIR ? 2 : 1) * Cfg::STAGE_BYTES);
           uint8_t* a = sA + stage * Cfg::A_BYTES;
           uint8_t* b = sB + stage * Cfg::B_BYTES;
-          if (!A_MN) {
-            tma_load_3d(a, &tmA, &full[stage], kb * BK, m_blk * BM, z);
-          } else {
+          if constexpr (PAIR) {
+            const uint32_t fb = full_cl0 + stage * 8;
+            if (!A_MN) {
+              tma_load_3d_pair(a, &tmA, fb, kb * BK, arow, z);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
-              tma_load_3d(a + j * 8192, &tmA, &full[stage], m_blk * BM + 64 * j, kb * BK, z);
-          }
-          if (!B_MN) {
-            tma_load_3d(b, &tmB, &full[stage], kb * BK, n_blk * BN, z);
-          } else {
+              for (int j = 0; j < BM / 64; ++j) tma_load_3d_pair(a + j * 8192, &tmA, fb, arow + 64 * j, kb * BK, z);
+            }
+            if (!B_MN) {
+              tma_load_3d_pair(b, &tmB, fb, kb * BK, brow, z);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j)
-              tma_load_3d(b + j * 8192, &tmB, &full[stage], n_blk * BN + 64 * j, kb * BK, z);
+              for (int j = 0; j < BN / 128; ++j) tma_load_3d_pair(b + j * 8192, &tmB, fb, brow + 64 * j, kb * BK, z);
+            }
+          } else {
+            if (!A_MN) {
+              tma_load_3d(a, &tmA, &full[stage], kb * BK, arow, z);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_3d(a + j * 8192, &tmA, &full[stage], arow + 64 * j, kb * BK, z);
+            }
+            if (!B_MN) {
+              tma_load_3d(b, &tmB, &full[stage], kb * BK, brow, z);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j)
+                tma_load_3d(b + j * 8192, &tmB, &full[stage], brow + 64 * j, kb * BK, z);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ------------------------------------------------ MMA issuer
-      constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
+    if (lane == 0 && rank == 0) {
+      // ------------------------------------------------ MMA issuer (the leader in PAIR mode)
+      constexpr uint32_t idesc = idesc_bf16(TM, BN, A_MN ? 1 : 0, B_MN ? 1 : 0);
       int stage = 0; uint32_t phase = 0;
       int acc = 0; uint32_t acc_phase = 0;
       WorkIter it(g);
@@ -225,12 +261,15 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                      : smem_desc_sw128(a_addr + k * 32, 16, 1024);
             const uint64_t bd = B_MN ? smem_desc_sw128(b_addr + k * 2048, 8192, 1024)
                                      : smem_desc_sw128(b_addr + k * 32, 16, 1024);
-            umma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            if constexpr (PAIR) umma_f16_pair(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+            else umma_f16(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           }
-          umma_commit(&empty[stage]);
+          if constexpr (PAIR) umma_commit_pair(&empty[stage], 0x3);   // frees the stage in both CTAs
+          else umma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        umma_commit(&tfull[acc]);
+        if constexpr (PAIR) umma_commit_pair(&tfull[acc], 0x3);
+        else umma_commit(&tfull[acc]);
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -240,6 +279,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int half = (warp - 2) / 4;         // the two warps of a quarter take alternate column boxes
     int acc = 0; uint32_t acc_phase = 0;
     uint8_t* stage_base = sOut + (warp - 2) * 4096;
+    const uint32_t tempty_cl0 = PAIR ? mapa_shared(&tempty[0], 0) : 0;
     WorkIter it(g);
     int t, kb0, kb1;
     while (it.next<BN>(g, t, kb0, kb1)) {
@@ -249,7 +289,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const bool have_acc = kb1 > kb0;
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row0 = m_blk * BM + quarter * 32;
+      const int row0 = m_blk * (PAIR ? 2 * BM : BM) + (int)rank * BM + quarter * 32;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
       if (g.tma_out) {
         // TMEM -> registers -> 128B-swizzled staging box (32 rows x 128 B) -> TMA
@@ -359,15 +399,20 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
       }
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      if constexpr (PAIR) mbar_arrive_cluster(tempty_cl0 + acc * 8);   // the leader's barrier
+      else mbar_arrive(&tempty[acc]);
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
     if (lane == 0) bulk_wait_all();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync();      // both CTAs done with the pair's TMEM before it is freed
+  else __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_dealloc_pair<Cfg::TMEM_COLS>(tmem_base);
+    else tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+  }
 }
 
 // ----------------------------------------------------------- fp32 SIMT GEMM
@@ -473,28 +518,44 @@ static int pick_bn(const mp_gemm_desc& g) {
   return 256;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, bool PAIR>
 static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                              const CUtensorMap& tc2, const TcArgs& a, int grid, cudaStream_t st) {
-  using Cfg = TcCfg<BN>;
-  auto k = tc_gemm_kernel<BN, A_MN, B_MN>;
+  using Cfg = TcCfg<BN, PAIR>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN, PAIR>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tc2, a);
-  return cudaGetLastError();
+  if constexpr (PAIR) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(GEMM_THREADS);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = 2;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, ta, tb, tc, tc2, a);
+  } else {
+    k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tc2, a);
+    return cudaGetLastError();
+  }
 }
 
-template <int BN>
+template <int BN, bool PAIR>
 static cudaError_t dispatch_major(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                                   const CUtensorMap& tc2, const TcArgs& a, int grid, int am, int bm, cudaStream_t st) {
-  if (!am && !bm) return launch_tc<BN, false, false>(ta, tb, tc, tc2, a, grid, st);
-  if (!am && bm) return launch_tc<BN, false, true>(ta, tb, tc, tc2, a, grid, st);
-  if (am && !bm) return launch_tc<BN, true, false>(ta, tb, tc, tc2, a, grid, st);
-  return launch_tc<BN, true, true>(ta, tb, tc, tc2, a, grid, st);
+  if (!am && !bm) return launch_tc<BN, false, false, PAIR>(ta, tb, tc, tc2, a, grid, st);
+  if (!am && bm) return launch_tc<BN, false, true, PAIR>(ta, tb, tc, tc2, a, grid, st);
+  if (am && !bm) return launch_tc<BN, true, false, PAIR>(ta, tb, tc, tc2, a, grid, st);
+  return launch_tc<BN, true, true, PAIR>(ta, tb, tc, tc2, a, grid, st);
 }
 
 // CTA budget of the next persistent GEMM launches (0 = every SM): lets a GEMM
@@ -503,6 +564,7 @@ static int g_max_ctas = 0;
 void gemm_set_max_ctas(int n) { g_max_ctas = n; }
 static int sm_cap() { return g_max_ctas > 0 ? std::min(g_max_ctas, num_sms()) : num_sms(); }
 static int tc_grid(const TcArgs& a) {
+  if (a.pair) return a.stream_k ? 2 * (sm_cap() / 2) : 2 * std::max(1, std::min(a.num_tiles, sm_cap() / 2));
   if (a.stream_k) return sm_cap();
   return std::max(1, std::min(a.num_tiles, sm_cap()));
 }
@@ -510,7 +572,7 @@ static int tc_grid(const TcArgs& a) {
 // last wave less than ~90% full and every CTA still gets >= 8 k-blocks.
 static bool want_stream_k(const TcArgs& a) {
   if (!a.accumulate || !a.tma_out || a.bias || a.causal) return false;
-  const int G = sm_cap();
+  const int G = a.pair ? sm_cap() / 2 : sm_cap();   // CTA pairs walk the work together
   if (a.num_tiles <= 0) return false;
   const long long waves = (a.num_tiles + G - 1) / G;
   const double fill = (double)a.num_tiles / (double)(waves * G);
@@ -526,12 +588,6 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
       (g.strideB * 2) % 16)
     return set_err(MP_EINVAL, "gemm: TMA needs 16-byte aligned operands and strides");
   const int BN = pick_bn(g);
-  CUtensorMap ta, tb;
-  bool ok = g.a_major ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.strideA, BK)
-                      : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.strideA, BM);
-  ok = ok && (g.b_major ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.strideB, BK)
-                        : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.strideB, BN));
-  if (!ok) return set_err(MP_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
   TcArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.batch = g.batch;
   a.m_blocks = (g.M + BM - 1) / BM;
@@ -540,6 +596,7 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   a.C = g.C; a.ldc = g.ldc; a.strideC = g.strideC;
   a.bias = reinterpret_cast<const __nv_bfloat16*>(g.bias);
   a.c_fp32 = g.c_fp32; a.accumulate = g.accumulate; a.causal = g.causal; a.alpha = g.alpha;
+  a.pair = 0;
   const int esz = g.c_fp32 ? 4 : 2;
   a.vec_ok = al16(g.C) && (g.ldc * esz) % 16 == 0 && (g.strideC * esz) % 16 == 0;
   CUtensorMap tc;
@@ -563,14 +620,37 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
     const double a_bytes = 2.0 * g.M * (double)g.K * g.batch, b_bytes = 2.0 * g.N * (double)g.K * g.batch;
     a.n_fast = (a.n_blocks > 1 && a_bytes > 2.0 * b_bytes && b_bytes < 32e6) ? 1 : 0;
   }
+  // CTA pairs (cta_group::2, 256 x BN tiles): halves each SM's B-operand traffic
+  // from L2.  GEMMs with >= 2 row blocks, BN >= 128, TMA epilogue, and >= 60
+  // GFLOP: interleaved A/B timing (scratch/pair_ab.py, wg_ab.py) has the pair
+  // 3-23 % faster on the layer and logit GEMMs of >= 65 GFLOP and up to 14 %
+  // slower on single-wave GEMMs below ~45 GFLOP.
+  const bool no_pair = getenv("MP_GEMM_NO_PAIR") != nullptr;   // read per call (A/B timing)
+  const double flop = 2.0 * g.M * (double)g.N * g.K * g.batch;
+  if (!no_pair && !g.causal && BN >= 128 && a.m_blocks >= 2 && a.tma_out && (sm_cap() % 2) == 0 && flop >= 60e9) {
+    a.pair = 1;
+    a.m_blocks = (g.M + 2 * BM - 1) / (2 * BM);
+    a.num_tiles = a.m_blocks * a.n_blocks * g.batch;
+  }
   a.stream_k = 0;
   static const bool no_sk = getenv("MP_GEMM_NO_STREAMK") != nullptr;
   a.stream_k = want_stream_k(a) && !no_sk;
+  CUtensorMap ta, tb;
+  bool ok = g.a_major ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.strideA, BK)
+                      : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.strideA, BM);
+  ok = ok && (g.b_major ? make_map(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.strideB, BK)
+                        : make_map(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.strideB, a.pair ? BN / 2 : BN));
+  if (!ok) return set_err(MP_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
   const int grid = tc_grid(a);
   cudaError_t e;
-  if (BN == 64) e = dispatch_major<64>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
-  else if (BN == 128) e = dispatch_major<128>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
-  else e = dispatch_major<256>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+  if (a.pair) {
+    if (BN == 128) e = dispatch_major<128, true>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+    else e = dispatch_major<256, true>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+  } else {
+    if (BN == 64) e = dispatch_major<64, false>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+    else if (BN == 128) e = dispatch_major<128, false>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+    else e = dispatch_major<256, false>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
+  }
   if (e != cudaSuccess) return set_err(MP_ECUDA, "gemm launch: %s", cudaGetErrorString(e));
   return MP_OK;
 }

@@ -187,3 +187,19 @@ def test_gemm_gelu_epilogue_rejects_fp32():
     d.act = 1
     with pytest.raises(mp.MPError):
         mp.mp_op_gemm("fp32", d)
+
+
+@pytest.mark.parametrize("am,bm", [(0, 0), (0, 1), (1, 1)])
+def test_gemm_bf16_cta_pair(am, bm):
+    """>= 60 GFLOP GEMMs run on CTA pairs (tcgen05.mma.cta_group::2, 256-row
+    tiles, each CTA loading half of B); ragged M and N included."""
+    got, ref = run_gemm(2048 + 136, 6912 - 64, 2304, 1, am, bm)
+    assert normwise(got, ref) < 1e-2
+
+
+@pytest.mark.parametrize("am,bm", [(1, 1), (0, 1)])
+def test_gemm_bf16_cta_pair_stream_k_accumulate(am, bm):
+    """Weight-gradient GEMMs >= 60 GFLOP: CTA pairs walking stream-K ranges,
+    partial tiles reduce-added into the fp32 accumulator."""
+    got, ref = run_gemm(6912, 2304, 2048, 1, am, bm, c_fp32=True, accumulate=True)
+    assert normwise(got, ref) < 1e-4
