@@ -63,6 +63,9 @@ def parse():
     ap.add_argument("--tp", dest="t", type=int, default=0, help="tensor parallel size (default: N / p)")
     ap.add_argument("--pp", dest="p", type=int, default=1, help="pipeline parallel size")
     ap.add_argument("--vp", dest="v", type=int, default=1, help="model chunks per device (interleaved)")
+    ap.add_argument("--dp", dest="d", type=int, default=1, help="data-parallel replicas (P:85-89)")
+    ap.add_argument("--recompute", action="store_true",
+                    help="activation recomputation (P:268-272); FLOPs then follow Eq. (2)'s 96-formula")
     ap.add_argument("--layers", type=int, default=0, help="override l (depth-reduced proxy; reported)")
     ap.add_argument("--B", type=int, default=16, help="global batch (sequences)")
     ap.add_argument("--b", type=int, default=1, help="microbatch size")
@@ -267,16 +270,19 @@ def bubble_report(st, world, p, v, m, sched):
 
 
 def workload_config(args, cfg):
-    t = args.t or max(1, args.gpus // args.p)
+    t = args.t or max(1, args.gpus // (args.p * args.d))
     sched = args.sched or ("interleaved" if args.v > 1 else "1f1b")
     return {"workload": f"GPT-{args.model} full training iteration (fwd+bwd all layers, flush, Adam)",
             "model": f"GPT-{args.model}", "l": cfg.l, "h": cfg.h, "a": cfg.a, "seq_len": cfg.s, "V": cfg.V,
-            "global_batch": args.B, "micro_batch": args.b, "m": args.B // args.b, "t": t, "p": args.p,
-            "v": args.v, "d": 1, "schedule": sched, "parallelism": f"t{t}p{args.p}v{args.v}",
+            "global_batch": args.B, "micro_batch": args.b, "m": args.B // (args.b * args.d), "t": t, "p": args.p,
+            "v": args.v, "d": args.d, "schedule": sched,
+            "parallelism": f"t{t}p{args.p}v{args.v}" + (f"d{args.d}" if args.d > 1 else ""),
             "attention": {"fused": "fused tcgen05 flash kernel (scores never materialised)",
                           "unfused": "paper: strided-batched scores GEMM + fused causal softmax + P.V GEMM"}[args.attn],
             "l2": "working set > 126 MB L2 every step (weights alone exceed it); no flush",
-            "flop_formula": "Eq. (2) 72-variant (no recomputation): 72Bslh^2(1+s/6h)+6BshV"}
+            "recompute": bool(args.recompute),
+            "flop_formula": ("Eq. (2) with recomputation: 96Bslh^2(1+s/6h+V/16lh)" if args.recompute else
+                             "Eq. (2) 72-variant (no recomputation): 72Bslh^2(1+s/6h)+6BshV")}
 
 
 def main():
@@ -295,16 +301,18 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", init_method="env://", device_id=torch.device("cuda", local))
-    t = args.t or max(1, world // args.p)
+    d = args.d
+    t = args.t or max(1, world // (args.p * d))
     p, v = args.p, args.v
     sched = args.sched or ("interleaved" if v > 1 else "1f1b")
     B, b = args.B, args.b
-    m = B // b
+    m = B // (b * d)
     # ---- context (NCCL id from rank 0, broadcast by the launcher)
     from paper_2104_04473_b200 import launch
     nid = launch.share_bytes(mp.mp_nccl_get_id() if rank == 0 else None, rank, world)
-    c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5, attn=args.attn, tp_comm=args.tp_comm)
-    ctx = mp.Context(t, p, v, 1, c, rank, world, local, nid)
+    c = mp.make_cfg(cfg.l, cfg.h, cfg.a, cfg.s, cfg.V, dtype="bf16", lr=1e-5, attn=args.attn, tp_comm=args.tp_comm,
+                    recompute=args.recompute)
+    ctx = mp.Context(t, p, v, d, c, rank, world, local, nid)
     # ---- random-init weights (only the owned shards are kept)
     dev_of, _ = mp.mp_get_stage_map(cfg.l, p, v)
     pp = (rank // t) % p
@@ -319,7 +327,7 @@ def main():
     d_tok = torch.tensor(tok, dtype=torch.int32, device="cuda")
     d_loss = torch.zeros(1, dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(ctx.stream())
-    F = mp.mp_flops(B, cfg.s, cfg.l, cfg.h, cfg.V, False)
+    F = mp.mp_flops(B, cfg.s, cfg.l, cfg.h, cfg.V, args.recompute)
     F96 = mp.mp_flops(B, cfg.s, cfg.l, cfg.h, cfg.V, True)
     # ---- warm-up (also yields the bubble statistics of one batch)
     wstats = None

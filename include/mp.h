@@ -44,7 +44,7 @@ typedef enum {
   MP_ECUDA = 6,         /* CUDA error or no usable sm_100 device */
   MP_ENCCL = 7,         /* NCCL error */
   MP_ESTATE = 8,        /* call order (e.g. layer call before mp_set_weights) */
-  MP_EUNSUPPORTED = 9   /* valid in the paper but not built here (e.g. d > 1) */
+  MP_EUNSUPPORTED = 9   /* valid in the paper but not built here (e.g. NVLS forced without multicast) */
 } mp_status;
 
 typedef enum { MP_GPIPE = 0, MP_1F1B = 1, MP_INTERLEAVED = 2 } mp_schedule;
@@ -70,7 +70,10 @@ typedef struct {
                             keyed by `seed` and each element's global (sequence, position, feature /
                             head, query, key) coordinates, regenerated in the backward (reading #6) */
   float ln_eps;          /* LayerNorm epsilon (reading #2: 1e-5) */
-  int recompute;         /* activation recomputation; counted by mp_flops only in round 1 */
+  int recompute;         /* activation recomputation: mp_run_batch keeps only each layer's
+                            input [s, b, h] between a microbatch's forward and backward task and re-runs
+                            the layer forward right before its backward (checkpoint every layer); the
+                            batch FLOP count becomes Eq. (2)'s 96-formula */
   unsigned long long seed;  /* dropout stream key */
   float lr;              /* Adam learning rate for mp_run_batch(apply_optimizer=1) */
   int attn_impl;         /* 0: the paper's attention core -- strided-batched scores GEMM, fused
@@ -140,8 +143,10 @@ mp_status mp_nccl_get_id(void* out);
  * builds the TP communicator, the four directed pipeline channels per rank
  * (activations to / from the neighbours, gradients to / from) and the
  * tied-embedding communicator, allocates this rank's weight shards (bf16 or
- * fp32), fp32 gradient accumulators and fp32 Adam state.  d > 1 returns
- * MP_EUNSUPPORTED in this round. */
+ * fp32), fp32 gradient accumulators and fp32 Adam state.  d > 1 (data
+ * parallelism) adds a communicator over the d replicas of each
+ * (pp, tp) shard; mp_run_batch sums the replicas' gradients with one
+ * ncclAllReduce at the pipeline flush. */
 mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world_rank, int world_size,
                   int local_device, const void* nccl_id, mp_ctx** out);
 mp_status mp_finalize(mp_ctx* ctx);
@@ -182,7 +187,8 @@ mp_status mp_layer_bwd(mp_ctx* ctx, int layer, int b, int stash_slot, const void
 
 /* One training iteration of B sequences under `sched`:
  * m = B/(b d) microbatches of b sequences; tokens host int32 [B, s+1]
- * (inputs tok[:, :s], labels tok[:, 1:]); every rank passes the same tokens.
+ * (inputs tok[:, :s], labels tok[:, 1:]); every rank passes the same tokens;
+ * data-parallel replica dp (d > 1) trains on rows [dp B/d, (dp+1) B/d).
  * Executes this rank's static task order (mp_get_schedule) with P2P
  * transfers on FIFO channels, flushes, all-reduces the tied
  * embedding gradient between the first and last stage, and, if

@@ -92,7 +92,6 @@ mp_status validate_cfg(const mp_model_cfg* c, int t, int p, int v, int d) {
   if ((4 * c->h) % t || c->h % t) return set_err(MP_EDIV, "h %% t != 0");
   if (c->V % t) return set_err(MP_EDIV, "V %% t != 0 (V=%d t=%d)", c->V, t);
   if (c->l % (p * v)) return set_err(MP_EDIV, "l %% (p v) != 0 (l=%d p=%d v=%d)", c->l, p, v);
-  if (d != 1) return set_err(MP_EUNSUPPORTED, "data parallelism d > 1 is not built in this round");
   return MP_OK;
 }
 

@@ -179,6 +179,7 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
   c->t = t; c->p = p; c->v = v; c->d = d; c->rank = world_rank; c->world = world_size; c->device = local_device;
   c->tp = world_rank % t;
   c->pp = (world_rank / t) % p;
+  c->dp = world_rank / (t * p);
   c->cfg = *cfg;
   if (c->cfg.ln_eps <= 0.f) c->cfg.ln_eps = 1e-5f;
   c->esz = cfg->dtype == MP_BF16 ? 2 : 4;
@@ -213,15 +214,21 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
   ncclResult_t r = ncclCommInitRank(&c->world_comm, world_size, id, world_rank);
   if (r != ncclSuccess) { delete c; return set_err(MP_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)); }
   if (t > 1) {
-    r = ncclCommSplit(c->world_comm, c->pp, c->tp, &c->tp_comm, nullptr);
+    r = ncclCommSplit(c->world_comm, c->dp * p + c->pp, c->tp, &c->tp_comm, nullptr);
     if (r != ncclSuccess) return set_err(MP_ENCCL, "tp split: %s", ncclGetErrorString(r));
   }
   if (p > 1) {
     // tied word embedding: stage 0 and stage S-1 hold copies of E_r (pipeline
     // activations / gradients travel over the IPC channels of p2p.cu)
     const bool tie = c->pp == 0 || c->pp == p - 1;
-    r = ncclCommSplit(c->world_comm, tie ? c->tp : NCCL_SPLIT_NOCOLOR, c->pp == 0 ? 0 : 1, &c->emb_comm, nullptr);
+    r = ncclCommSplit(c->world_comm, tie ? c->dp * t + c->tp : NCCL_SPLIT_NOCOLOR, c->pp == 0 ? 0 : 1, &c->emb_comm,
+                      nullptr);
     if (r != ncclSuccess) return set_err(MP_ENCCL, "embedding split: %s", ncclGetErrorString(r));
+  }
+  if (d > 1) {
+    // data parallelism: replicas of the same (pp, tp) shard sum their gradients
+    r = ncclCommSplit(c->world_comm, c->pp * t + c->tp, c->dp, &c->dp_comm, nullptr);
+    if (r != ncclSuccess) return set_err(MP_ENCCL, "dp split: %s", ncclGetErrorString(r));
   }
   // ---- stage map and parameters
   c->dev_of_layer.resize(cfg->l);
@@ -269,7 +276,7 @@ mp_status mp_finalize(mp_ctx* c) {
   cudaStreamSynchronize(c->cs);
   p2p_release(c);
   tp_sym_free(c);
-  ncclComm_t comms[] = {c->tp_comm, c->emb_comm, c->world_comm};
+  ncclComm_t comms[] = {c->tp_comm, c->emb_comm, c->dp_comm, c->world_comm};
   for (auto cm : comms)
     if (cm) ncclCommDestroy(cm);
   void* bufs[] = {c->ws_z, c->ws_dsq, c->ws_d4h, c->ws_dh1, c->ws_dh2, c->ws_dqkv, c->ws_dctx, c->ws_ln, c->ws_fa,
@@ -404,17 +411,21 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   const size_t act_elems = (size_t)s * b * h, act_bytes = act_elems * c->esz;
   const float scale = 1.f / ((float)B * (float)s);
   cudaStream_t cs = c->cs;
+  const bool recompute = c->cfg.recompute != 0;
 
   MP_TRY(p2p_ensure(c, act_bytes));
   cudaEvent_t ev_start = X.timing.get(), ev_end = X.timing.get();
   MP_CUDA(cudaEventRecord(ev_start, cs));
   // tokens -> device (inputs x = tok[:, :s], labels y = tok[:, 1:])
+  // this data-parallel replica's rows [dp B/d, (dp+1) B/d) of the batch
+  const size_t rows = (size_t)m * b;
+  const int* tok_mine = tokens + (size_t)c->dp * rows * (s + 1);
   int* dtok = nullptr;
   if (tok_dev) {
-    dtok = const_cast<int*>(tokens);
+    dtok = const_cast<int*>(tok_mine);
   } else {
-    MP_TRY(alloc_async(c, (void**)&dtok, sizeof(int) * (size_t)B * (s + 1), cs));
-    MP_CUDA(cudaMemcpyAsync(dtok, tokens, sizeof(int) * (size_t)B * (s + 1), cudaMemcpyHostToDevice, cs));
+    MP_TRY(alloc_async(c, (void**)&dtok, sizeof(int) * rows * (s + 1), cs));
+    MP_CUDA(cudaMemcpyAsync(dtok, tok_mine, sizeof(int) * rows * (s + 1), cudaMemcpyHostToDevice, cs));
   }
   MP_CUDA(cudaMemsetAsync(c->grads, 0, (size_t)c->n_params * 4, cs));
   MP_CUDA(cudaMemsetAsync(c->d_loss, 0, 4, cs));
@@ -431,7 +442,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
     if (dbg) fprintf(stderr, "[mp rank %d] enqueue %c mb=%d chunk=%d stage=%d\n", c->rank, tk.kind ? 'B' : 'F', tk.mb,
                      tk.chunk, sigma);
     const int* tok = dtok + (size_t)tk.mb * b * (s + 1);
-    c->cur_seq0 = tk.mb * b;        // global index of the microbatch's first sequence (dropout counters)
+    c->cur_seq0 = (c->dp * m + tk.mb) * b;   // global index of the microbatch's first sequence (dropout counters)
     if (tk.kind == 0) {
       // ------------------------------------------------------------ forward
       void* x = nullptr;
@@ -456,6 +467,10 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
         LayerStash ls;
         ls.x = x; ls.own_x = true;
         MP_TRY(layer_fwd(c, k, b, x, y, ls));
+        if (recompute) {    // activation recomputation: keep only the layer input
+          MP_CUDA(cudaFreeAsync(ls.block, cs));
+          ls.block = nullptr;
+        }
         stash[{tk.mb, k}] = ls;
         x = y;
       }
@@ -501,6 +516,12 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
         void* dx = nullptr;
         MP_TRY(alloc_async(c, &dx, act_bytes, cs));
         LayerStash& ls = stash.at({tk.mb, k});
+        if (recompute) {    // re-run the layer forward from its checkpointed input (one extra forward)
+          void* y = nullptr;
+          MP_TRY(alloc_async(c, &y, act_bytes, cs));
+          MP_TRY(layer_fwd(c, k, b, ls.x, y, ls));
+          MP_CUDA(cudaFreeAsync(y, cs));
+        }
         MP_TRY(layer_bwd(c, k, ls, dy, dx));
         MP_TRY(stash_release(c, ls, cs));
         stash.erase({tk.mb, k});
@@ -544,7 +565,11 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
                         "embedding grad all-reduce"));
     }
   }
-  // loss: contributed by (last stage, tp 0) only, then shared with every rank
+  // data parallelism: sum the replicas' gradients (each already carries the 1/(B s) global-batch scale)
+  if (c->dp_comm)
+    MP_TRY(nccl_check(ncclAllReduce(c->grads, c->grads, (size_t)c->n_params, ncclFloat32, ncclSum, c->dp_comm, cs),
+                      "data-parallel gradient all-reduce"));
+  // loss: contributed by (last stage, tp 0) of every replica, then shared with every rank
   {
     const bool contrib = c->has_head && c->tp == 0;
     float* red = c->d_loss + 32;

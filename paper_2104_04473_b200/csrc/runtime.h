@@ -51,12 +51,13 @@ struct HeadStash {
 
 struct mp_ctx {
   // process grid, rank = (dp * p + pp) * t + tp
-  int t, p, v, d, rank, world, tp, pp, device;
+  int t, p, v, d, rank, world, tp, pp, dp, device;
   mp_model_cfg cfg;
   int esz;                       // storage element size
   ncclDataType_t nccl_dt;
   // communicators
   ncclComm_t world_comm = nullptr, tp_comm = nullptr, emb_comm = nullptr;
+  ncclComm_t dp_comm = nullptr;   // same (pp, tp) across the d replicas (d > 1): gradient all-reduce at the flush
   // streams
   cudaStream_t cs = nullptr, side = nullptr, s_act_send = nullptr, s_act_recv = nullptr, s_grad_send = nullptr,
                s_grad_recv = nullptr;

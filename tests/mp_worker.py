@@ -33,6 +33,8 @@ def main():
     ap.add_argument("--attn", default="unfused")
     ap.add_argument("--pdrop", type=float, default=0.0)
     ap.add_argument("--tpcomm", default="auto")
+    ap.add_argument("--dp", dest="d", type=int, default=1)
+    ap.add_argument("--recompute", type=int, default=0)
     ap.add_argument("--out", default="")
     # arguments come through MP_WORKER_ARGS: torchrun's own parser would
     # otherwise claim any option that prefixes one of its flags (--m, --t ...)
@@ -52,26 +54,28 @@ def main():
     dist.broadcast_object_list(nid, src=0)
     shape = gen.ModelCfg(l=a.l, h=a.h, a=4, s=32 if a.attn == "unfused" else 64, V=512)
     W = gen.model_weights(shape, seed=42, dtype=a.dtype)
-    tok = gen.tokens(a.m, shape.s, shape.V, seed=1234)
+    tok = gen.tokens(a.m * a.d, shape.s, shape.V, seed=1234)   # the global batch; replica dp takes its rows
     cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype, attn=a.attn,
-                      p_drop_attn=a.pdrop, p_drop_hidden=a.pdrop, seed=4321, tp_comm=a.tpcomm)
-    ctx = mp.Context(a.t, a.p, a.v, 1, cfg, rank, world, local, nid[0])
+                      p_drop_attn=a.pdrop, p_drop_hidden=a.pdrop, seed=4321, tp_comm=a.tpcomm,
+                      recompute=bool(a.recompute))
+    ctx = mp.Context(a.t, a.p, a.v, a.d, cfg, rank, world, local, nid[0])
     tp, pp = rank % a.t, (rank // a.t) % a.p
     tol = {"bf16": 2e-2, "fp32": 1e-4}[a.dtype]
-    report = {"rank": rank, "tp": tp, "pp": pp, "errors": {}}
+    report = {"rank": rank, "tp": tp, "pp": pp, "dp": rank // (a.t * a.p), "errors": {}}
     try:
         for k, Wl in enumerate(W["layers"]):
             for name, arr in Wl.items():
                 ctx.set_weights(name, k, arr)
         for name in ("emb", "pos", "lnf_g", "lnf_b"):
             ctx.set_weights(name, 0, W[name])
-        loss, stats = ctx.run_batch(a.m, 1, a.m, a.sched, tok)
+        loss, stats = ctx.run_batch(a.m * a.d, 1, a.m, a.sched, tok)
         masks = None
         if a.pdrop > 0:
             from oracle import philox as PH
             masks = [[PH.layer_masks(4321, k, [i], shape.s, shape.h, shape.a, a.pdrop, a.pdrop)
-                      for k in range(shape.l)] for i in range(a.m)]
-        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m, masks=masks)
+                      for k in range(shape.l)] for i in range(a.m * a.d)]
+        # the oracle runs the whole global batch in one process: d replicas x m microbatches
+        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m * a.d, masks=masks)
         report["loss"] = [loss, lr]
         report["stats"] = stats
         report["tp_comm"] = ctx.tp_comm_mode()

@@ -78,7 +78,9 @@ def test_validate():
     assert mp.mp_validate(cfg, 5, 1, 1, 1) == mp.MP_EDIV          # a % t
     assert mp.mp_validate(cfg, 2, 3, 1, 1) == mp.MP_EDIV          # l % (p v)
     assert mp.mp_validate(cfg, 2, 4, 2, 1, 38, 1, "interleaved") == mp.MP_ESCHED   # m % p
-    assert mp.mp_validate(cfg, 2, 4, 1, 2) == mp.MP_EUNSUPPORTED
+    assert mp.mp_validate(cfg, 2, 4, 1, 2) == mp.MP_OK             # d > 1
+    assert mp.mp_validate(cfg, 2, 4, 1, 2, 64, 1, "1f1b") == mp.MP_OK
+    assert mp.mp_validate(cfg, 2, 4, 1, 2, 66, 2, "1f1b") == mp.MP_EDIV   # B % (b d)
 
 
 def test_compute_call_without_gpu_fails_loudly():

@@ -149,3 +149,43 @@ def test_pipeline_channels_gloo(p, v, m, kind):
         for k, gl in mine.items():
             for name, val in gl.items():
                 assert np.max(np.abs(val - g["layers"][k][name])) <= 1e-12 * max(1e-300, np.max(np.abs(val))), (k, name)
+
+
+def _worker_dp(rank, world, port, q):
+    """Data-parallel replica `rank` (t = p = 1, d = world): the runtime's
+    convention -- replica dp trains on rows [dp B/d, (dp+1) B/d), scales its
+    loss by 1/(B s) of the GLOBAL batch and the flush sums the replicas'
+    gradients -- must reproduce the whole-batch gradient."""
+    _init(rank, world, port)
+    shape = gen.TINY
+    W = gen.model_weights(shape, seed=42, dtype="fp32")
+    m = 2
+    tok = gen.tokens(m * world, shape.s, shape.V, seed=1234)
+    dp = launch.tp_pp_of(rank, 1, 1)[2]
+    mine = tok[dp * m:(dp + 1) * m]
+    loss, g = M.batch_fwd_bwd(W, mine, shape.a, m)          # mean over this replica's m*s tokens
+    flat = np.concatenate([g["emb"].ravel()] + [v.ravel() for Wl in g["layers"] for v in Wl.values()])
+    t_ = torch.tensor(np.append(flat, loss) / world, dtype=torch.float64)   # -> 1/(B s) of the global batch
+    dist.all_reduce(t_)
+    q.put((rank, t_.numpy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_data_parallel_gradient_sum(world):
+    ctx = mp_.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_dp, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    out = sorted((q.get(timeout=300) for _ in range(world)), key=lambda x: x[0])
+    for p in ps:
+        p.join(60)
+    shape = gen.TINY
+    W = gen.model_weights(shape, seed=42, dtype="fp32")
+    tok = gen.tokens(2 * world, shape.s, shape.V, seed=1234)
+    loss, g = M.batch_fwd_bwd(W, tok, shape.a, 2 * world)
+    ref = np.append(np.concatenate([g["emb"].ravel()] + [v.ravel() for Wl in g["layers"] for v in Wl.values()]), loss)
+    for _, got in out:
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-15 * np.abs(ref).max())

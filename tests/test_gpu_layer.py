@@ -211,3 +211,46 @@ def test_run_batch_dropout(dtype, attn, h):
             assert normwise(ctx.get_grads(name, 0).reshape(gr[name].shape), gr[name]) < tol, name
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("dtype,attn,h,pd", [("fp32", "unfused", 64, 0.0), ("bf16", "unfused", 64, 0.1),
+                                             ("bf16", "fused", 128, 0.1)])
+def test_run_batch_recompute(dtype, attn, h, pd):
+    """Activation recomputation: same loss and gradients as the
+    oracle (and bit-identical to the stashing run), FLOP count = Eq. (2)'s
+    96-formula (P:349-352)."""
+    from oracle import formulas as F
+    from oracle import philox as PH
+    shape = gen.ModelCfg(l=4, h=h, a=4, s=32 if attn == "unfused" else 64, V=512)
+    m = 4
+    W = gen.model_weights(shape, seed=42, dtype=dtype)
+    tok = gen.tokens(m, shape.s, shape.V, seed=1234)
+    res = {}
+    for rc in (0, 1):
+        c = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=dtype, attn=attn, p_drop_attn=pd,
+                        p_drop_hidden=pd, seed=99, recompute=bool(rc))
+        ctx = mp.Context(1, 1, 2, 1, c, 0, 1, 0, mp.mp_nccl_get_id())
+        try:
+            load_model(ctx, W)
+            loss, stats = ctx.run_batch(m, 1, m, "interleaved", tok)
+            grads = {(name, k): ctx.get_grads(name, k) for k in range(shape.l) for name in W["layers"][k]}
+            res[rc] = (loss, grads, stats)
+        finally:
+            ctx.close()
+    masks = None
+    if pd > 0:
+        masks = [[PH.layer_masks(99, k, [i], shape.s, shape.h, shape.a, pd, pd) for k in range(shape.l)]
+                 for i in range(m)]
+    lr, gr = M.batch_fwd_bwd(W, tok, shape.a, m, masks=masks)
+    loss, grads, stats = res[1]
+    tol = TOL[dtype]
+    assert abs(loss - lr) / abs(lr) < tol
+    for (name, k), g in grads.items():
+        ref = gr["layers"][k][name]
+        assert normwise(g.reshape(ref.shape), ref) < tol, (k, name)
+        # recomputation replays the same kernels on the same inputs (only the order of the
+        # fp32 gradient reduce-adds may differ)
+        assert normwise(g, res[0][1][(name, k)]) < 1e-5, (k, name)
+    assert abs(res[1][0] - res[0][0]) <= 1e-6 * abs(res[0][0])
+    assert stats["model_flops"] == float(F.flops(m, shape.s, shape.l, shape.h, shape.V, True))
+    assert res[0][2]["model_flops"] == float(F.flops(m, shape.s, shape.l, shape.h, shape.V, False))

@@ -141,3 +141,54 @@ def test_multi_gpu_nvls_shot_variants(tmp_path, t, shot, dtype):
     msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
     assert r.returncode == 0, msg
     assert len(reps) == t and all(x["ok"] for x in reps), msg
+
+
+def _run_worker(tmp_path, n, args, port_base, key):
+    out = str(tmp_path / "rep")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port_base + (hash(key) % 2000)}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    env = dict(os.environ, MP_WORKER_ARGS=f"{args} --out {out}")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
+    msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
+    assert r.returncode == 0, msg
+    assert len(reps) == n and all(x["ok"] for x in reps), msg
+    return reps
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+@pytest.mark.parametrize("t,p,v,d,m,sched", [
+    (1, 1, 1, 2, 2, "1f1b"),
+    (2, 1, 1, 2, 2, "1f1b"),
+    (1, 2, 1, 2, 2, "1f1b"),
+    (1, 2, 2, 2, 2, "interleaved"),
+])
+def test_multi_gpu_data_parallel(tmp_path, t, p, v, d, m, sched, dtype):
+    """Data parallelism: d replicas each run m microbatches of their
+    rows of the global batch; after the flush's gradient all-reduce every
+    replica's shards equal the oracle's gradient of the whole batch (B = m d)."""
+    n = t * p * d
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    reps = _run_worker(tmp_path, n, f"--tp {t} --pp {p} --vp {v} --dp {d} --m {m} --sched {sched} --dtype {dtype}",
+                       39000, (t, p, v, d, m, sched, dtype))
+    assert len({round(x["loss"][0], 6) for x in reps}) == 1
+    assert sorted({x["dp"] for x in reps}) == list(range(d))
+
+
+@pytest.mark.parametrize("t,p,v,m,sched,attn,pdrop", [
+    (2, 2, 2, 4, "interleaved", "unfused", 0.0),
+    (2, 1, 1, 4, "1f1b", "fused", 0.1),
+    (1, 2, 1, 4, "1f1b", "fused", 0.0),
+])
+def test_multi_gpu_recompute(tmp_path, t, p, v, m, sched, attn, pdrop):
+    """Activation recomputation: only each layer's input survives
+    the forward task; the backward re-runs the layer forward (incl. its g
+    reductions and regenerated dropout masks) and still equals the oracle."""
+    n = t * p
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    h = 128 if attn == "fused" else 64
+    _run_worker(tmp_path, n, f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype bf16 --h {h} "
+                f"--l {max(4, p * v)} --attn {attn} --pdrop {pdrop} --recompute 1", 41000, (t, p, v, m, sched, attn))
