@@ -40,6 +40,11 @@ extern "C" {
  * act = 1 (bf16 only; the fused bias-GeLU of a15): C = x, C2 = gelu(x)
  *   with x = alpha A B + bias in fp32, both bf16 [M, N] with ldc / strideC
  *   (tanh form of GeLU, as in the oracle); act = 0: C2 unused.
+ * act = 2 (bf16 only; the GeLU backward of a17 fused into the FC2 dgrad GEMM):
+ *   C = bf16(x * gelu'(C2)) with x = alpha A B in fp32 and C2 the stored bf16
+ *   pre-activation U [M, N] (same ldc / strideC); if colsum != NULL, also
+ *   colsum[n] += sum_m C[m, n] (of the stored bf16 values: the FC1 bias
+ *   gradient), fp32 atomics.  No bias, no accumulate.
  * bf16 runs on the tcgen05 tensor cores (TMA-fed, TMEM accumulators);
  * fp32 runs a SIMT FFMA kernel (tcgen05 has no fp32 kind). */
 typedef struct {
@@ -55,6 +60,7 @@ typedef struct {
   float alpha;
   int act;
   void* C2;
+  float* colsum;
 } mp_gemm_desc;
 
 mp_status mp_op_gemm(mp_dtype dtype, const mp_gemm_desc* g, void* stream);

@@ -61,7 +61,9 @@ struct TcArgs {
   int tma_out;          // epilogue through shared memory + TMA store / reduce-add (tmC valid)
   int stream_k;         // accumulate mode: CTAs split the (tile, k-block) iterations evenly
   int n_fast;           // tile order n-block fastest (consecutive tiles share the A panel)
-  int act;              // 1: bf16 C = x and C2 = gelu(x) (tmC2 valid)
+  int act;              // 1: bf16 C = x and C2 = gelu(x) (tmC2 valid); 2: C = x * gelu'(U), U = aux
+  const __nv_bfloat16* aux;   // act 2: pre-activation U, same layout as C
+  float* colsum;        // act 2: colsum[n] += sum_m C[m, n] (optional)
   int pair;             // CTA-pair kernel: m_blocks count 256-row pair tiles
   int kb_per_tile;      // k-blocks per tile (stream_k)
   float alpha;
@@ -84,6 +86,13 @@ __device__ __forceinline__ float gelu_fast(float u) {
   float th;
   asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(0.7978845608028654f * (u + 0.044715f * u * u * u)));
   return 0.5f * u * (1.f + th);
+}
+// d gelu / du, tanh form (oracle.layer.gelu_grad)
+__device__ __forceinline__ float dgelu_fast(float u) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  float th;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(c * (u + a * u * u * u)));
+  return 0.5f * (1.f + th) + 0.5f * u * (1.f - th * th) * c * (1.f + 3.f * a * u * u);
 }
 
 // Work sequence of one CTA, identical for the producer, MMA and epilogue roles.
@@ -167,7 +176,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     if (g.tma_out) tma_prefetch(&tmC);
-    if (g.act) tma_prefetch(&tmC2);
+    if (g.act == 1) tma_prefetch(&tmC2);
   }
   if (warp == 1) {
     if constexpr (PAIR) tmem_alloc_pair<Cfg::TMEM_COLS>(tmem_slot);
@@ -334,8 +343,37 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 x[32 * hf + c] = a0;
               }
             }
+            if (g.act == 2) {
+              // GeLU backward: x *= gelu'(U) for this lane's row (64 contiguous bf16 = 128 B)
+              const int row = row0 + lane;
+              const __nv_bfloat16* U = g.aux + (long long)z * g.strideC + (long long)row * g.ldc + col0;
+              const bool full = col0 + 64 <= g.N;
+#pragma unroll
+              for (int chunk = 0; chunk < 8; ++chunk) {
+                uint4 q = make_uint4(0, 0, 0, 0);
+                if (row < g.M) {
+                  if (full) q = __ldg(reinterpret_cast<const uint4*>(U) + chunk);
+                  else {
+                    uint32_t w[4] = {0, 0, 0, 0};
+                    for (int e = 0; e < 8; ++e)
+                      if (col0 + 8 * chunk + e < g.N) {
+                        const uint16_t hv = reinterpret_cast<const uint16_t*>(U)[8 * chunk + e];
+                        w[e / 2] |= (uint32_t)hv << (16 * (e & 1));
+                      }
+                    q = make_uint4(w[0], w[1], w[2], w[3]);
+                  }
+                }
+                const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  __nv_bfloat162 pr = *reinterpret_cast<const __nv_bfloat162*>(&qw[e]);
+                  x[8 * chunk + 2 * e] *= dgelu_fast(__low2float(pr));
+                  x[8 * chunk + 2 * e + 1] *= dgelu_fast(__high2float(pr));
+                }
+              }
+            }
             // pass 0: x (the output, or the pre-activation when act); pass 1 (act): gelu(x)
-            for (int pass = 0; pass < (g.act ? 2 : 1); ++pass) {
+            for (int pass = 0; pass < (g.act == 1 ? 2 : 1); ++pass) {
               if (pass == 1) {
                 // the pre-activation box goes out first, then GeLU reuses the staging buffer
                 fence_proxy_async_smem();
@@ -356,16 +394,59 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 for (int e = 0; e < 4; ++e) {
                   __nv_bfloat162 pr = __floats2bfloat162_rn(x[8 * chunk + 2 * e], x[8 * chunk + 2 * e + 1]);
                   w[e] = *reinterpret_cast<uint32_t*>(&pr);
+                  if (g.act == 2) {   // the column sum is of the stored (rounded) values
+                    x[8 * chunk + 2 * e] = __low2float(pr);
+                    x[8 * chunk + 2 * e + 1] = __high2float(pr);
+                  }
                 }
                 st_shared_v4(rowaddr + ((chunk ^ (lane & 7)) << 4), w[0], w[1], w[2], w[3]);
               }
+            }
+            if (g.act == 2 && g.colsum) {
+              // column sums of the 32 x 64 box: butterfly reduce-scatter over the warp
+              // (halving the live columns each step), then 2 columns per lane -> fp32 atomics
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                const bool hi = lane & 16;
+                const float send = hi ? x[j] : x[j + 32], keep = hi ? x[j + 32] : x[j];
+                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+              }
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const bool hi = lane & 8;
+                const float send = hi ? x[j] : x[j + 16], keep = hi ? x[j + 16] : x[j];
+                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const bool hi = lane & 4;
+                const float send = hi ? x[j] : x[j + 8], keep = hi ? x[j + 8] : x[j];
+                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const bool hi = lane & 2;
+                const float send = hi ? x[j] : x[j + 4], keep = hi ? x[j + 4] : x[j];
+                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+              }
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const bool hi = lane & 1;
+                const float send = hi ? x[j] : x[j + 2], keep = hi ? x[j + 2] : x[j];
+                x[j] = keep + __shfl_xor_sync(0xffffffffu, send, 1);
+              }
+              const int cl = 32 * ((lane >> 4) & 1) + 16 * ((lane >> 3) & 1) + 8 * ((lane >> 2) & 1) +
+                             4 * ((lane >> 1) & 1) + 2 * (lane & 1);
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+                if (col0 + cl + j < g.N) atomicAdd(g.colsum + col0 + cl + j, x[j]);
             }
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             if (g.accumulate) tma_reduce_add_3d(&tmC, buf, col0, row0, z);
-            else tma_store_3d(g.act ? &tmC2 : &tmC, buf, col0, row0, z);
+            else tma_store_3d(g.act == 1 ? &tmC2 : &tmC, buf, col0, row0, z);
             bulk_commit();
           }
         }
@@ -606,7 +687,12 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   CUtensorMap tc2;
   memset(&tc2, 0, sizeof(tc2));
   a.act = g.act;
-  if (g.act) {
+  a.aux = reinterpret_cast<const __nv_bfloat16*>(g.C2);
+  a.colsum = g.colsum;
+  if (g.act == 2) {
+    if (g.c_fp32 || g.accumulate || g.bias || !a.tma_out || !g.C2 || g.causal)
+      return set_err(MP_EINVAL, "gemm: act 2 needs bf16 C, the pre-activation C2, no bias / accumulate");
+  } else if (g.act) {
     if (g.c_fp32 || g.accumulate || !a.tma_out || !al16(g.C2) ||
         !make_map(&tc2, g.C2, g.N, g.M, g.batch, g.ldc, g.strideC, 32, esz))
       return set_err(MP_EINVAL, "gemm: act needs bf16 C / C2, 16-byte aligned, no accumulate");

@@ -86,6 +86,18 @@ static mp_status lin_dgrad(mp_ctx* c, const void* dY, const void* W, void* dX, i
   g.c_fp32 = c->cfg.dtype == MP_FP32;
   return gemm(c->cfg.dtype, g, c->cs);
 }
+// dU[T, K] = (dY[T, N] W[N, K]) * gelu'(U) and db[K] += colsum(dU): the FC2 dgrad GEMM with the
+// GeLU backward and the FC1 bias gradient in its epilogue (bf16)
+static mp_status lin_dgrad_dgelu(mp_ctx* c, const void* dY, const void* W, const void* U, void* dU, float* db, int T,
+                                 int N, int K) {
+  mp_gemm_desc g{};
+  g.M = T; g.N = K; g.K = N; g.batch = 1;
+  g.A = dY; g.lda = N; g.a_major = 0;
+  g.B = W; g.ldb = K; g.b_major = 1;
+  g.C = dU; g.ldc = K; g.alpha = 1.f;
+  g.act = 2; g.C2 = const_cast<void*>(U); g.colsum = db;
+  return gemm(c->cfg.dtype, g, c->cs);
+}
 void gemm_set_max_ctas(int n);
 // dW[N, K] += dY[T, N]^T X[T, K]  (fp32 accumulators)
 static mp_status lin_wgrad(mp_ctx* c, const void* dY, const void* X, float* dW, int T, int N, int K,
@@ -332,10 +344,14 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   } else {
     MP_TRY(colsum_accum<T>(dY, gptr(c, lp[P_B2]), d.T, d.h, c->cs));
   }
-  MP_TRY(lin_dgrad(c, dZ2, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
-  MP_TRY(lin_wgrad(c, dZ2, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
-  MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, fuse_gelu(c) ? nullptr : ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]),
-                          d.T, d.h4t, c->cs));
+  if (fuse_gelu(c)) {      // Y1 holds the biased pre-activation; GeLU backward + db1 in the dgrad epilogue
+    MP_TRY(lin_dgrad_dgelu(c, dZ2, ptr<T>(c, lp[P_W2]), st.Y1, dU, gptr(c, lp[P_B1]), d.T, d.h, d.h4t));
+    MP_TRY(lin_wgrad(c, dZ2, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
+  } else {
+    MP_TRY(lin_dgrad(c, dZ2, ptr<T>(c, lp[P_W2]), dU, d.T, d.h, d.h4t));
+    MP_TRY(lin_wgrad(c, dZ2, st.H, gptr(c, lp[P_W2]), d.T, d.h, d.h4t));
+    MP_TRY(bias_gelu_bwd<T>(dU, (const T*)st.Y1, ptr<T>(c, lp[P_B1]), dU, gptr(c, lp[P_B1]), d.T, d.h4t, c->cs));
+  }
   // f (a17): NVLS -- dgrad writes its partial into the symmetric buffer, dW1 accumulates, one barrier,
   // and the LayerNorm backward reduce-loads the sum; NCCL -- all-reduce dA2 on the side stream during dW1
   const bool nv = c->tps.on, two = nv && tp_sym_two_shot(c), nvr = nv && !two && !tp_sym_debug_local();

@@ -64,7 +64,7 @@ class GemmDesc(ctypes.Structure):
                 ("C", ctypes.c_void_p), ("ldc", ctypes.c_longlong), ("strideC", ctypes.c_longlong),
                 ("bias", ctypes.c_void_p), ("c_fp32", ctypes.c_int), ("accumulate", ctypes.c_int),
                 ("causal", ctypes.c_int), ("alpha", ctypes.c_float), ("act", ctypes.c_int),
-                ("C2", ctypes.c_void_p)]
+                ("C2", ctypes.c_void_p), ("colsum", ctypes.c_void_p)]
 
 
 _lib = None

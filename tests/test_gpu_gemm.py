@@ -180,6 +180,43 @@ def test_gemm_bf16_gelu_epilogue(M, N, K):
     assert normwise(host(H), gelu(ref_u)) < 1e-2
 
 
+@pytest.mark.parametrize("M,N,K,colsum", [(2048, 9216, 2304, True), (2048, 1152, 2304, True), (304, 520, 200, True),
+                                          (96, 1000, 136, False)])
+def test_gemm_bf16_dgelu_epilogue(M, N, K, colsum):
+    """act = 2: the FC2 dgrad GEMM writes dU = (dY W) * gelu'(U) and adds the
+    column sums of dU (the FC1 bias gradient) into an fp32 accumulator (a17).
+    Shapes include the 1.7B t=1 / t=8 MLP widths (CTA-pair kernel) and ragged
+    M, N."""
+    from oracle.layer import gelu_grad
+    A = gen.activations((1, M, K), 17, 1.0, "bf16")
+    Bt = gen.activations((1, N, K), 18, 1.0, "bf16")
+    Uh = gen.activations((M, N), 19, 1.0, "bf16")
+    dA, dB, dU_in = dev(A, "bf16"), dev(Bt, "bf16"), dev(Uh, "bf16")
+    out = torch.zeros((M, N), dtype=torch.bfloat16, device="cuda")
+    acc0 = gen.activations((N,), 20, 1.0, "fp32")
+    db = dev(acc0, "fp32")
+    d = mp.GemmDesc()
+    d.M, d.N, d.K, d.batch = M, N, K, 1
+    d.A, d.lda, d.strideA = dA.data_ptr(), K, M * K
+    d.B, d.ldb, d.strideB = dB.data_ptr(), K, N * K
+    d.C, d.ldc, d.strideC = out.data_ptr(), N, M * N
+    d.alpha = 1.0
+    d.act = 2
+    d.C2 = dU_in.data_ptr()
+    d.colsum = db.data_ptr() if colsum else None
+    mp.mp_op_gemm("bf16", d)
+    torch.cuda.synchronize()
+    ref = gemm_ref(A, np.swapaxes(Bt, 1, 2), 1.0, None)[0] * gelu_grad(Uh)
+    got = host(out)
+    assert normwise(got, ref) < 1e-2
+    if colsum:
+        # the sum of the stored values, accumulated onto the previous contents
+        assert normwise(host(db) - acc0, got.astype(np.float64).sum(axis=0)) < 1e-4
+        assert normwise(host(db) - acc0, ref.sum(axis=0)) < 1e-2
+    else:
+        assert np.array_equal(host(db), acc0.astype(np.float32).astype(np.float64))
+
+
 def test_gemm_gelu_epilogue_rejects_fp32():
     d = mp.GemmDesc()
     d.M = d.N = d.K = 64
