@@ -68,7 +68,9 @@ def parse():
                     help="activation recomputation (P:268-272); FLOPs then follow Eq. (2)'s 96-formula")
     ap.add_argument("--layers", type=int, default=0, help="override l (depth-reduced proxy; reported)")
     ap.add_argument("--B", type=int, default=16, help="global batch (sequences)")
-    ap.add_argument("--b", type=int, default=1, help="microbatch size")
+    ap.add_argument("--b", type=int, default=2,
+                    help="microbatch size (default 2: the best of the b in {1, 2, 4} sweep at 1.7B on 1xB200, "
+                         "the paper's own tuning knob, P:259-266, P:492)")
     ap.add_argument("--sched", default="", help="gpipe | 1f1b | interleaved (default: 1f1b, interleaved if v > 1)")
     ap.add_argument("--attn", default="fused", choices=["fused", "unfused"],
                     help="attention core: fused tcgen05 flash kernel (default) or the paper's unfused "

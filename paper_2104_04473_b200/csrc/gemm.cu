@@ -329,6 +329,28 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                            __float_as_uint(v[2]), __float_as_uint(v[3]));
             }
           } else {
+            uint4 uq[8];
+            if (g.act == 2) {   // all 8 loads in flight before any use
+              const int row = row0 + lane;
+              const __nv_bfloat16* U = g.aux + (long long)z * g.strideC + (long long)row * g.ldc + col0;
+              const bool full = col0 + 64 <= g.N && row < g.M;
+              if (full) {
+#pragma unroll
+                for (int chunk = 0; chunk < 8; ++chunk) uq[chunk] = __ldg(reinterpret_cast<const uint4*>(U) + chunk);
+              } else {
+#pragma unroll
+                for (int chunk = 0; chunk < 8; ++chunk) {
+                  uint32_t w[4] = {0, 0, 0, 0};
+                  if (row < g.M)
+                    for (int e = 0; e < 8; ++e)
+                      if (col0 + 8 * chunk + e < g.N) {
+                        const uint16_t hv = reinterpret_cast<const uint16_t*>(U)[8 * chunk + e];
+                        w[e / 2] |= (uint32_t)hv << (16 * (e & 1));
+                      }
+                  uq[chunk] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+              }
+            }
             float x[64];
 #pragma unroll
             for (int hf = 0; hf < 2; ++hf) {
@@ -344,25 +366,11 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               }
             }
             if (g.act == 2) {
-              // GeLU backward: x *= gelu'(U) for this lane's row (64 contiguous bf16 = 128 B)
-              const int row = row0 + lane;
-              const __nv_bfloat16* U = g.aux + (long long)z * g.strideC + (long long)row * g.ldc + col0;
-              const bool full = col0 + 64 <= g.N;
+              // GeLU backward: x *= gelu'(U) for this lane's row (64 contiguous bf16 = 128 B,
+              // loaded before the TMEM reads above so the latency overlaps them)
 #pragma unroll
               for (int chunk = 0; chunk < 8; ++chunk) {
-                uint4 q = make_uint4(0, 0, 0, 0);
-                if (row < g.M) {
-                  if (full) q = __ldg(reinterpret_cast<const uint4*>(U) + chunk);
-                  else {
-                    uint32_t w[4] = {0, 0, 0, 0};
-                    for (int e = 0; e < 8; ++e)
-                      if (col0 + 8 * chunk + e < g.N) {
-                        const uint16_t hv = reinterpret_cast<const uint16_t*>(U)[8 * chunk + e];
-                        w[e / 2] |= (uint32_t)hv << (16 * (e & 1));
-                      }
-                    q = make_uint4(w[0], w[1], w[2], w[3]);
-                  }
-                }
+                const uint4 q = uq[chunk];
                 const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {

@@ -229,6 +229,7 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
     // data parallelism: replicas of the same (pp, tp) shard sum their gradients
     r = ncclCommSplit(c->world_comm, c->pp * t + c->tp, c->dp, &c->dp_comm, nullptr);
     if (r != ncclSuccess) return set_err(MP_ENCCL, "dp split: %s", ncclGetErrorString(r));
+    MP_CUDA(cudaStreamCreateWithPriority(&c->s_dp, cudaStreamNonBlocking, lo));
   }
   // ---- stage map and parameters
   c->dev_of_layer.resize(cfg->l);
@@ -287,7 +288,7 @@ mp_status mp_finalize(mp_ctx* c) {
   for (auto e : c->events) cudaEventDestroy(e);
   auto it = g_extra.find(c);
   if (it != g_extra.end()) { it->second.sync.destroy(); it->second.timing.destroy(); g_extra.erase(it); }
-  cudaStream_t ss[] = {c->cs, c->side, c->s_act_send, c->s_act_recv, c->s_grad_send, c->s_grad_recv};
+  cudaStream_t ss[] = {c->cs, c->side, c->s_act_send, c->s_act_recv, c->s_grad_send, c->s_grad_recv, c->s_dp};
   for (auto s : ss)
     if (s) cudaStreamDestroy(s);
   delete c;
@@ -435,6 +436,15 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> task_ev;
   int inflight = 0, peak = 0;
   mp_status st = MP_OK;
+  // data parallelism: once a layer's last backward (its m-th) is enqueued, its gradient
+  // segment is all-reduced over the replicas on s_dp while the remaining layers' backward
+  // runs.  Only at t = 1: with t > 1 the TP reductions are spinning kernels / NCCL kernels
+  // of another communicator whose relative order across ranks would not be fixed.
+  const bool dp_overlap = c->dp_comm && c->t == 1 && !getenv("MP_DP_NO_OVERLAP");
+  std::map<int, int> bwd_count;
+  long long model_off = c->n_params;   // first model-level (emb / pos / lnf) element; layers precede it
+  for (const auto& P : c->params)
+    if (P.layer < 0) model_off = std::min(model_off, P.off);
 
   static const bool dbg = getenv("MP_DEBUG") != nullptr;
   for (const Task& tk : tasks) {
@@ -523,6 +533,15 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
           MP_CUDA(cudaFreeAsync(y, cs));
         }
         MP_TRY(layer_bwd(c, k, ls, dy, dx));
+        if (dp_overlap && ++bwd_count[k] == m) {
+          const auto& ix = c->layer_params.at(k).idx;
+          const long long lo = c->params[ix[0]].off, hi = c->params[ix[11]].off + c->params[ix[11]].numel;
+          cudaEvent_t e = X.sync.get();
+          MP_CUDA(cudaEventRecord(e, cs));
+          MP_CUDA(cudaStreamWaitEvent(c->s_dp, e, 0));
+          MP_TRY(nccl_check(ncclAllReduce(c->grads + lo, c->grads + lo, (size_t)(hi - lo), ncclFloat32, ncclSum,
+                                          c->dp_comm, c->s_dp), "data-parallel layer gradient all-reduce"));
+        }
         MP_TRY(stash_release(c, ls, cs));
         stash.erase({tk.mb, k});
         MP_CUDA(cudaFreeAsync(dy, cs));
@@ -566,9 +585,18 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
     }
   }
   // data parallelism: sum the replicas' gradients (each already carries the 1/(B s) global-batch scale)
-  if (c->dp_comm)
-    MP_TRY(nccl_check(ncclAllReduce(c->grads, c->grads, (size_t)c->n_params, ncclFloat32, ncclSum, c->dp_comm, cs),
-                      "data-parallel gradient all-reduce"));
+  if (c->dp_comm) {
+    long long lo = 0;
+    if (dp_overlap) {   // the layers' segments are already in flight on s_dp
+      cudaEvent_t e = X.sync.get();
+      MP_CUDA(cudaEventRecord(e, c->s_dp));
+      MP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+      lo = model_off;
+    }
+    if (c->n_params > lo)
+      MP_TRY(nccl_check(ncclAllReduce(c->grads + lo, c->grads + lo, (size_t)(c->n_params - lo), ncclFloat32, ncclSum,
+                                      c->dp_comm, cs), "data-parallel gradient all-reduce"));
+  }
   // loss: contributed by (last stage, tp 0) of every replica, then shared with every rank
   {
     const bool contrib = c->has_head && c->tp == 0;

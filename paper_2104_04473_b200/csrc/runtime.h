@@ -61,6 +61,7 @@ struct mp_ctx {
   // streams
   cudaStream_t cs = nullptr, side = nullptr, s_act_send = nullptr, s_act_recv = nullptr, s_grad_send = nullptr,
                s_grad_recv = nullptr;
+  cudaStream_t s_dp = nullptr;   // d > 1: per-layer gradient all-reduces overlapping the last backward passes
   cudaMemPool_t pool = nullptr;
   // stage map
   std::vector<int> dev_of_layer, chunk_of_layer;
