@@ -408,13 +408,15 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   uint8_t* sdS = sP + T_BYTES;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sdS + T_BYTES);
   uint64_t* kv_full = bar + 0;
-  uint64_t* qd_full = bar + 1;
-  uint64_t* qd_empty = bar + 2;
+  uint64_t* q_full = bar + 1;     // Q_i landed
+  uint64_t* q_empty = bar + 2;    // Q_i's last products (dK += dS^T Q_i) complete
+  uint64_t* do_full = bar + 7;    // dO_i landed
+  uint64_t* do_empty = bar + 9;   // dO_i's last products (dV += P^T dO_i) complete
   uint64_t* sdp_full = bar + 3;
   uint64_t* ds_ready = bar + 4;
   uint64_t* dq_full = bar + 5;
   uint64_t* tmem_free = bar + 6;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 10);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // key/value tile, heaviest (most query tiles) first across the whole grid;
@@ -432,7 +434,8 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   const int tile_bytes = g.nhb * 128 * 128;
 
   if (threadIdx.x == 0) {
-    mbar_init(kv_full, 1); mbar_init(qd_full, 1); mbar_init(qd_empty, 1); mbar_init(sdp_full, 1);
+    mbar_init(kv_full, 1); mbar_init(q_full, 1); mbar_init(q_empty, 1); mbar_init(sdp_full, 1);
+    mbar_init(do_full, 1); mbar_init(do_empty, 1);
     mbar_init(ds_ready, CW); mbar_init(dq_full, 1); mbar_init(tmem_free, CW);
     fence_mbar_init();
   }
@@ -454,12 +457,14 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       }
       for (int it = 0; it < niter; ++it) {
         const int qi = kt + it0 + it;
-        if (it > 0) mbar_wait(qd_empty, (it - 1) & 1);
-        mbar_arrive_expect_tx(qd_full, 2 * tile_bytes);
-        for (int hb = 0; hb < g.nhb; ++hb) {
-          tma_load_3d(sQ + hb * 16384, &tmQ, qd_full, 64 * hb, qi * 128, z);
-          tma_load_3d(sdO + hb * 16384, &tmdO, qd_full, 64 * hb, qi * 128, z);
-        }
+        // dO_i as soon as the dV products of i-1 are done, Q_i after its dK products
+        // (the MMA issuer runs the dV products first): the loads overlap the tail of i-1
+        if (it > 0) mbar_wait(do_empty, (it - 1) & 1);
+        mbar_arrive_expect_tx(do_full, tile_bytes);
+        for (int hb = 0; hb < g.nhb; ++hb) tma_load_3d(sdO + hb * 16384, &tmdO, do_full, 64 * hb, qi * 128, z);
+        if (it > 0) mbar_wait(q_empty, (it - 1) & 1);
+        mbar_arrive_expect_tx(q_full, tile_bytes);
+        for (int hb = 0; hb < g.nhb; ++hb) tma_load_3d(sQ + hb * 16384, &tmQ, q_full, 64 * hb, qi * 128, z);
         FA_TRACE(0, it);
       }
     }
@@ -473,34 +478,41 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const uint32_t aQ = smem_u32(sQ), aK = smem_u32(sK), aV = smem_u32(sV), adO = smem_u32(sdO);
       const uint32_t aP = smem_u32(sP), adS = smem_u32(sdS);
       for (int it = 0; it < niter; ++it) {
-        mbar_wait(qd_full, it & 1);
         if (it > 0) mbar_wait(tmem_free, (it - 1) & 1);
+        mbar_wait(do_full, it & 1);
         tc_fence_after();
-        for (int k = 0; k < kh; ++k) {       // K-major operands over hd
+        for (int k = 0; k < kh; ++k) {       // dP = dO V^T (K-major operands over hd)
+          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
+          umma_f16(tmem + 128, smem_desc_sw128(adO + off, 16, 1024), smem_desc_sw128(aV + off, 16, 1024), id_sdp,
+                   k > 0 ? 1u : 0u);
+        }
+        mbar_wait(q_full, it & 1);
+        tc_fence_after();
+        for (int k = 0; k < kh; ++k) {       // S = Q K^T
           const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
           umma_f16(tmem + 0, smem_desc_sw128(aQ + off, 16, 1024), smem_desc_sw128(aK + off, 16, 1024), id_sdp,
-                   k > 0 ? 1u : 0u);
-          umma_f16(tmem + 128, smem_desc_sw128(adO + off, 16, 1024), smem_desc_sw128(aV + off, 16, 1024), id_sdp,
                    k > 0 ? 1u : 0u);
         }
         umma_commit(sdp_full);
         FA_TRACE(1, it);
         mbar_wait(ds_ready, it & 1);
         tc_fence_after();
-        for (int k = 0; k < 8; ++k) {        // reductions over the 128 query rows / 128 keys
-          const uint32_t mn = k * 2048;                                  // MN-major view: K rows step
-          const uint32_t km = (k / 4) * 16384 + (k % 4) * 32;             // K-major view
-          // dV += P^T dO ; dK += dS^T Q
-          umma_f16(tmem + 256, smem_desc_sw128(aP + mn, 16384, 1024), smem_desc_sw128(adO + mn, 16384, 1024), id_dkv,
-                   (it > 0 || k > 0) ? 1u : 0u);
-          umma_f16(tmem + 384, smem_desc_sw128(adS + mn, 16384, 1024), smem_desc_sw128(aQ + mn, 16384, 1024), id_dkv,
-                   (it > 0 || k > 0) ? 1u : 0u);
-          // dQ_i = dS K  (into the dP columns, already consumed)
-          umma_f16(tmem + 128, smem_desc_sw128(adS + km, 16, 1024), smem_desc_sw128(aK + mn, 16384, 1024), id_dq,
+        // reductions over the 128 query rows / 128 keys; MN-major views step K rows by 2 KB,
+        // K-major views step 16 columns.  dV first (frees dO_i), then dK (frees Q_i), then dQ.
+        for (int k = 0; k < 8; ++k)          // dV += P^T dO
+          umma_f16(tmem + 256, smem_desc_sw128(aP + k * 2048, 16384, 1024), smem_desc_sw128(adO + k * 2048, 16384, 1024),
+                   id_dkv, (it > 0 || k > 0) ? 1u : 0u);
+        umma_commit(do_empty);
+        for (int k = 0; k < 8; ++k)          // dK += dS^T Q
+          umma_f16(tmem + 384, smem_desc_sw128(adS + k * 2048, 16384, 1024), smem_desc_sw128(aQ + k * 2048, 16384, 1024),
+                   id_dkv, (it > 0 || k > 0) ? 1u : 0u);
+        umma_commit(q_empty);
+        for (int k = 0; k < 8; ++k) {        // dQ_i = dS K  (into the dP columns, already consumed)
+          const uint32_t km = (k / 4) * 16384 + (k % 4) * 32;
+          umma_f16(tmem + 128, smem_desc_sw128(adS + km, 16, 1024), smem_desc_sw128(aK + k * 2048, 16384, 1024), id_dq,
                    k > 0 ? 1u : 0u);
         }
         umma_commit(dq_full);
-        umma_commit(qd_empty);
         FA_TRACE(2, it);
       }
     }
