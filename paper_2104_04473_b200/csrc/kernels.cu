@@ -110,6 +110,14 @@ static int row_threads(int nvec) {
   return std::max(32, std::min(256, t));
 }
 constexpr int LN_MAXV = 4;
+// Grid of a row kernel: every row handled by one CTA in a grid-stride loop, the grid
+// sized to the CTAs that are resident at once (<= 64 warps / 32 CTAs per SM), so there
+// is no partial last wave (T = 4096 rows of 96 threads would be 1.3 waves).
+static int row_grid(long long R, int nvec) {
+  const int warps = row_threads(nvec) / 32;
+  const int per_sm = std::max(1, std::min(32, 64 / warps));
+  return (int)std::max(1LL, std::min<long long>(R, (long long)num_sms() * per_sm));
+}
 
 #define LAUNCH_CHECK()                                                                         \
   do {                                                                                         \
@@ -126,11 +134,12 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, c
                                                      const T* __restrict__ res, T* __restrict__ x1,
                                                      const T* __restrict__ g, const T* __restrict__ b,
                                                      T* __restrict__ out, float* __restrict__ mean,
-                                                     float* __restrict__ rstd, int h, float eps, Dropout dp) {
+                                                     float* __restrict__ rstd, int h, float eps, Dropout dp, int R) {
   constexpr int V = VW<T>::N;
   __shared__ float2 red[32];
-  const long long row = blockIdx.x;
   const int nvec = h / V;
+  // grid-stride over rows: a grid of a few resident CTAs per SM, no partial last wave
+  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
   float v[LN_MAXV][V];
   float s1 = 0.f;
 #pragma unroll
@@ -183,6 +192,7 @@ __global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, c
     }
   }
   if (threadIdx.x == 0) { mean[row] = mu; rstd[row] = rs; }
+  }
 }
 
 template <class T>
@@ -197,8 +207,8 @@ template <class T>
 mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int R, int h, float eps,
                         cudaStream_t st) {
   MP_TRY(check_row_dims<T>(R, h));
-  ln_fwd_kernel<T, 0><<<R, row_threads(h / VW<T>::N), 0, st>>>(x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, h,
-                                                                eps, Dropout{});
+  ln_fwd_kernel<T, 0><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(
+      x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, h, eps, Dropout{}, R);
   LAUNCH_CHECK();
 }
 
@@ -208,9 +218,11 @@ mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const
                             bool red) {
   MP_TRY(check_row_dims<T>(R, h));
   if (red)
-    ln_fwd_kernel<T, 1, true><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp);
+    ln_fwd_kernel<T, 1, true><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(
+        yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp, R);
   else
-    ln_fwd_kernel<T, 1><<<R, row_threads(h / VW<T>::N), 0, st>>>(yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp);
+    ln_fwd_kernel<T, 1><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(
+        yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp, R);
   LAUNCH_CHECK();
 }
 
@@ -265,11 +277,11 @@ template <class T, bool RED = false>
 __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                         const T* __restrict__ g, const float* __restrict__ mean,
                                                         const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy) {
+                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy, int R) {
   constexpr int V = VW<T>::N;
   __shared__ float2 red[32];
-  const long long row = blockIdx.x;
   const int nvec = h / V;
+  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
   const float mu = mean[row], rs = rstd[row];
   float xh[LN_MAXV][V], dxh[LN_MAXV][V];
   float s1 = 0.f, s2 = 0.f;
@@ -308,6 +320,7 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy
       }
       st_vec(dx + row * h + vi * V, o);
     }
+  }
   }
 }
 
@@ -441,10 +454,12 @@ mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, 
                         cudaStream_t st, T* dy_copy) {
   MP_TRY(check_row_dims<T>(R, h));
   if (dy_copy) {
-    ln_bwd_dx_kernel<T, true><<<R, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, dy_copy);
+    ln_bwd_dx_kernel<T, true><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd,
+                                                                                               dres, dx, h, dy_copy, R);
     dy = dy_copy;
   } else {
-    ln_bwd_dx_kernel<T><<<R, row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, nullptr);
+    ln_bwd_dx_kernel<T><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx,
+                                                                                         h, nullptr, R);
   }
   count_launch();
   ln_bwd_gb_kernel<T><<<ct_grid(h / VW<T>::N, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dgamma, dbeta, R, h);
