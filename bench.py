@@ -164,13 +164,15 @@ def cpu_oracle_layer(cfg, reps=1):
     W = gen.layer_weights(h, cfg.l, seed=5, layer=0, dtype="bf16")
     X = gen.activations((s, 1, h), 6, 1.0, "bf16")
     dY = gen.activations((s, 1, h), 7, 1e-3, "bf16")
-    t0 = time.perf_counter()
-    for _ in range(reps):
-        _, cache = L.layer_fwd(X, W, a)
-        L.layer_bwd(dY, cache, W, a)
-    dt = time.perf_counter() - t0
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank; rank 0 runs this alone)
+    with threadpoolctl.threadpool_limits(limits=os.cpu_count() or 1):
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            _, cache = L.layer_fwd(X, W, a)
+            L.layer_bwd(dY, cache, W, a)
+        dt = time.perf_counter() - t0
+        info = threadpoolctl.threadpool_info()
     flops = reps * 3 * (24 * s * h * h + 4 * s * s * h)
-    info = threadpoolctl.threadpool_info()
     threads = max([i.get("num_threads", 1) for i in info] or [1])
     return flops, dt, threads
 
