@@ -14,6 +14,15 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
 
+def free_port():
+    """A port the OS reports free right now (hash-derived ports collided with sockets of
+    earlier torchrun launches still in TIME_WAIT: EADDRINUSE)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
 def ngpus():
     import torch
     return torch.cuda.device_count()
@@ -41,7 +50,7 @@ def test_multi_gpu_parity(tmp_path, t, p, v, m, sched, dtype):
         pytest.skip(f"needs {n} GPUs")
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={29500 + (hash((t, p, v, m, sched, dtype)) % 2000)}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype {dtype} --out {out}")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
@@ -61,7 +70,7 @@ def test_multi_gpu_parity_fused_attention(tmp_path, t, p, v, m, sched):
         pytest.skip(f"needs {n} GPUs")
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={31000 + (hash((t, p, v, m, sched)) % 2000)}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype bf16 "
                                           f"--h 128 --l {max(4, p * v)} --attn fused --out {out}")
@@ -81,7 +90,7 @@ def test_multi_gpu_parity_dropout(tmp_path, t, p, v, m, sched, attn):
         pytest.skip(f"needs {n} GPUs")
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={33000 + (hash((t, p, v, m, sched, attn)) % 2000)}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     h = 128 if attn == "fused" else 64
     env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype fp32 "
@@ -108,7 +117,7 @@ def test_multi_gpu_tp_transport(tmp_path, t, p, v, m, sched, tpcomm, dtype):
         pytest.skip(f"needs {n} GPUs")
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={35000 + (hash((t, p, v, m, sched, tpcomm, dtype)) % 2000)}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype {dtype} "
                                           f"--tpcomm {tpcomm} --out {out}")
@@ -131,7 +140,7 @@ def test_multi_gpu_nvls_shot_variants(tmp_path, t, shot, dtype):
         pytest.skip(f"needs {t} GPUs")
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={t}",
-           "--master-addr=127.0.0.1", f"--master-port={37000 + (hash((t, shot, dtype)) % 2000)}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MP_TP_NVLS_SHOT=shot,
                MP_WORKER_ARGS=f"--tp {t} --pp 1 --vp 1 --m 4 --sched 1f1b --dtype {dtype} --tpcomm nvls --out {out}")
@@ -146,7 +155,7 @@ def test_multi_gpu_nvls_shot_variants(tmp_path, t, shot, dtype):
 def _run_worker(tmp_path, n, args, port_base, key):
     out = str(tmp_path / "rep")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={port_base + (hash(key) % 2000)}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
     env = dict(os.environ, MP_WORKER_ARGS=f"{args} --out {out}")
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
