@@ -273,6 +273,43 @@ def bubble_report(st, world, p, v, m, sched):
     return rep
 
 
+def comm_calibration(cfg, b, t, p, d, world, m, t_step):
+    """NVLink roofline of the TP communication (t > 1, p = d = 1 so the TP group is the
+    world): one layer's g / f payload (s*b*h bf16) all-reduced by NCCL over the TP group,
+    CUDA events, after warm-up.  busbw = algbw * 2(t-1)/t against the 900 GB/s per-direction
+    NVLink 5 peak.  The library's default NVLS path fuses the reduction into the consuming
+    LayerNorm / residual kernel, so this is the calibration of the paper's transport and an
+    upper bound of the communication share (4 reductions per layer per microbatch)."""
+    if t <= 1 or p != 1 or d != 1 or world != t:
+        return None
+    import torch
+    import torch.distributed as dist
+    n = cfg.s * b * cfg.h
+    x = torch.ones(n, dtype=torch.bfloat16, device="cuda")
+    for _ in range(5):
+        dist.all_reduce(x)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    reps = 20
+    e0.record()
+    for _ in range(reps):
+        dist.all_reduce(x)
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / 1e3 / reps
+    from paper_2104_04473_b200 import launch
+    sec = launch.max_over_ranks(sec, world, "cuda")
+    algbw = 2.0 * n / sec / 1e9
+    busbw = algbw * 2.0 * (t - 1) / t
+    per_step = 4 * cfg.l * m
+    return {"payload_bytes": 2 * n, "nccl_allreduce_us": sec * 1e6, "algbw_gbs": algbw, "busbw_gbs": busbw,
+            "nvlink_peak_gbs": 900.0, "frac": busbw / 900.0, "reductions_per_step": per_step,
+            "nccl_share_of_step_upper_bound": per_step * sec / t_step,
+            "how": "torch NCCL all_reduce of one layer payload (s*b*h bf16) on the TP group, 20 reps after 5 "
+                   "warm-up, CUDA events, max over ranks; busbw = algbw*2(t-1)/t vs 900 GB/s NVLink 5 per "
+                   "direction; share = reductions * time / step (the NVLS default fuses them into consumers)"}
+
+
 def workload_config(args, cfg):
     t = args.t or max(1, args.gpus // (args.p * args.d))
     sched = args.sched or ("interleaved" if args.v > 1 else "1f1b")
@@ -427,6 +464,8 @@ def main():
         "clocks": clk,
         "bubble": bubble_report(wstats, world, p, v, m, sched),
     }
+    if world > 1:
+        out["comm"] = comm_calibration(cfg, b, t, p, d, world, m, t_step)
     if e2e:
         out["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -690,38 +690,47 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 // D[z, q] = sum_d dO[q, z, d] O[q, z, d]   (one warp per row)
 __global__ void flash_bwd_dot_kernel(const __nv_bfloat16* __restrict__ dO, const __nv_bfloat16* __restrict__ O,
                                      float* __restrict__ D, int s, int zn, int hd, long long ldo) {
-  const long long row = blockIdx.x * 8LL + threadIdx.x / 32;
-  const int lane = threadIdx.x % 32;
-  if (row >= (long long)zn * s) return;
-  const int z = (int)(row / s), q = (int)(row % s);
-  const __nv_bfloat162* a = reinterpret_cast<const __nv_bfloat162*>(dO + (long long)q * ldo + (long long)z * hd);
-  const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(O + (long long)q * ldo + (long long)z * hd);
+  // 16 lanes per row, one 16-byte vector (8 elements) per lane (hd <= 128); rows taken in
+  // memory order (q major, z minor), so a warp streams contiguous [q, z, hd] data
+  const long long row = (blockIdx.x * (long long)blockDim.x + threadIdx.x) / 16;   // = q * zn + z
+  const int j = threadIdx.x % 16;
+  const bool ok = row < (long long)zn * s;
   float acc = 0.f;
-  for (int c = lane; c < hd / 2; c += 32) {
-    const float2 x = __bfloat1622float2(a[c]), y = __bfloat1622float2(b[c]);
-    acc += x.x * y.x + x.y * y.y;
+  if (ok && 8 * j < hd) {
+    const long long off = (row / zn) * ldo + (row % zn) * hd + 8 * j;
+    const uint4 a = *reinterpret_cast<const uint4*>(dO + off), b = *reinterpret_cast<const uint4*>(O + off);
+    const __nv_bfloat162* pa = reinterpret_cast<const __nv_bfloat162*>(&a);
+    const __nv_bfloat162* pb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 x = __bfloat1622float2(pa[k]), y = __bfloat1622float2(pb[k]);
+      acc += x.x * y.x + x.y * y.y;
+    }
   }
 #pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) D[row] = acc;
+  for (int o = 8; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (ok && j == 0) D[(row % zn) * s + row / zn] = acc;
 }
 
 // dQacc fp32 [z, s, hd] -> bf16 Q slot of dQKV [s, b, heads, 3, hd]
-// (dQ: slot 0; split mode also dK: slot 1, dV: slot 2)
+// (dQ: slot 0; split mode also dK: slot 1, dV: slot 2); 8 elements per thread
 __global__ void flash_bwd_dq_kernel(const float* __restrict__ acc0, __nv_bfloat16* __restrict__ dQKV, int s, int zn,
                                     int hd, long long ldq, int slot0, long long slot_stride) {
   const int slot = slot0 + (int)blockIdx.y;        // destination slot; accumulators slot_stride floats apart
   const float* acc = acc0 + blockIdx.y * slot_stride;
-  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;   // one pair of elements
-  const long long n = (long long)zn * s * hd / 2;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;   // one group of 8 elements
+  const long long n = (long long)zn * s * hd / 8;
   if (i >= n) return;
-  const long long e = 2 * i;
+  const long long e = 8 * i;
   const int d = (int)(e % hd);
   const long long zq = e / hd;
   const int q = (int)(zq % s), z = (int)(zq / s);
-  const float2 v = *reinterpret_cast<const float2*>(acc + e);
-  *reinterpret_cast<__nv_bfloat162*>(dQKV + (long long)q * ldq + (long long)z * 3 * hd + slot * hd + d) =
-      __floats2bfloat162_rn(v.x, v.y);
+  const float4 v0 = *reinterpret_cast<const float4*>(acc + e), v1 = *reinterpret_cast<const float4*>(acc + e + 4);
+  uint4 u;
+  __nv_bfloat162* w = reinterpret_cast<__nv_bfloat162*>(&u);
+  w[0] = __floats2bfloat162_rn(v0.x, v0.y); w[1] = __floats2bfloat162_rn(v0.z, v0.w);
+  w[2] = __floats2bfloat162_rn(v1.x, v1.y); w[3] = __floats2bfloat162_rn(v1.z, v1.w);
+  *reinterpret_cast<uint4*>(dQKV + (long long)q * ldq + (long long)z * 3 * hd + slot * hd + d) = u;
 }
 
 // Split-Q work decomposition of the backward (few heads per rank, e.g. t >= 2):
@@ -807,7 +816,7 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   if (work) MP_CUDA(cudaMemsetAsync(dkacc, 0, sizeof(float) * 2 * zn * s * hd, st));
   {
     const long long rows = zn * s;
-    flash_bwd_dot_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(dO),
+    flash_bwd_dot_kernel<<<(unsigned)((rows + 15) / 16), 256, 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(dO),
                                                                    reinterpret_cast<const __nv_bfloat16*>(O), D, s,
                                                                    (int)zn, hd, ldo);
     count_launch();
@@ -844,7 +853,7 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   else flash_bwd_kernel<false><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
   count_launch();
   {
-    const long long n = zn * s * hd / 2;
+    const long long n = zn * s * hd / 8;
     if (work) {   // dQ, dK, dV (dK / dV accumulators are contiguous after D)
       flash_bwd_dq_kernel<<<dim3((unsigned)((n + 255) / 256), 1), 256, 0, st>>>(
           dqacc, reinterpret_cast<__nv_bfloat16*>(dQKV), s, (int)zn, hd, ldq, 0, 0);
