@@ -237,7 +237,7 @@ def replay_bubble(p, m, v, sched, tf, tb):
     return [(end[r] - busy[r]) / busy[r] for r in range(p)]
 
 
-def bubble_report(st, world, p, v, m, sched):
+def bubble_report(st, world, p, v, m, sched, d=1):
     """Per-rank pipeline idle share of the last warm-up batch (max over ranks) next to
     the closed form (p-1)/m or (p-1)/(v m), and the ideal-pipeline
     estimate from this run's own per-task durations (equal stages assumed)."""
@@ -261,8 +261,9 @@ def bubble_report(st, world, p, v, m, sched):
            "t_fwd_task_s": [round(r[3], 6) for r in per_rank], "t_bwd_task_s": [round(r[4], 6) for r in per_rank],
            "flush_and_optimizer_s": max(r[5] - r[1] for r in per_rank)}
     if p > 1:
-        # pipeline stage r = the ranks with pp = r (TP ranks of a stage behave alike: use the max)
-        t = world // p
+        # pipeline stage r = the ranks with pp = r in replica 0, rank = (dp p + pp) t + tp
+        # (TP ranks of a stage behave alike: use the max)
+        t = world // (p * d)
         tf = [max(per_rank[r * t + k][3] for k in range(t)) for r in range(p)]
         tb = [max(per_rank[r * t + k][4] for k in range(t)) for r in range(p)]
         rp = replay_bubble(p, m, v, sched, tf, tb)
@@ -462,7 +463,7 @@ def main():
         "gpu_launches": int(launches),
         "step_ms_rank0": [round(x, 3) for x in step_ms],
         "clocks": clk,
-        "bubble": bubble_report(wstats, world, p, v, m, sched),
+        "bubble": bubble_report(wstats, world, p, v, m, sched, d),
     }
     if world > 1:
         out["comm"] = comm_calibration(cfg, b, t, p, d, world, m, t_step)
