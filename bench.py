@@ -8,7 +8,7 @@ TFLOP/s by the paper's formula (Eq. (2)).
 
 Default workload (BASELINE.json configs[1], "GPT 1.7B, t=1..8, p=1"): GPT-1.7B
 (h=2304, a=24, l=24, s=2048, V=51200), tensor parallel t = N, p = 1, global
-batch B = 16 sequences of microbatch b = 1 (m = 16, 1F1B), bf16 storage with
+batch B = 16 sequences of microbatch b = 2 (m = 8, 1F1B), bf16 storage with
 fp32 accumulation, synthetic tokens and random-init weights.  Every step's
 working set (3.3 GB of bf16 weights alone) exceeds the 126 MB L2, so no L2
 flush is needed between steps.
@@ -16,8 +16,8 @@ flush is needed between steps.
 FLOP accounting: without activation recomputation the honest per-iteration
 count is the 72-variant of Eq. (2), 72 B s l h^2 (1 + s/6h) + 6 B s h V
 (reading #18); `value` uses it.  The 96-formula number is
-reported beside it for reference.  `value` is the whole-job aggregate over
-the N GPUs; `per_gpu_tflops` is the paper's per-GPU metric.
+reported beside it for reference.  `value` is the paper's metric, model
+TFLOP/s PER GPU (F / (N t_step)); `aggregate_tflops` is the whole-job sum.
 """
 import argparse
 import json
@@ -29,20 +29,27 @@ import time
 
 import numpy as np
 
-# stdout carries exactly one JSON line: library chatter (e.g. NCCL's version
-# banner printed from C) is sent to stderr, the JSON goes to the saved stdout
-_JSON_FD = os.dup(1)
-os.dup2(2, 1)
+_JSON_FD = None
+
+
+def redirect_stdout():
+    """stdout carries exactly one JSON line: library chatter (e.g. NCCL's version
+    banner printed from C) is sent to stderr, the JSON goes to the saved stdout.
+    Called from main() only, so importing this module has no side effects."""
+    global _JSON_FD
+    if _JSON_FD is None:
+        _JSON_FD = os.dup(1)
+        os.dup2(2, 1)
 
 
 def emit(obj):
     sys.stdout.flush()
-    os.write(_JSON_FD, (json.dumps(obj) + "\n").encode())
-
-# Enough hardware work queues that the compute stream's waits on P2P events
-# never sit in front of a channel stream's NCCL kernel (false dependencies
-# deadlock the pipeline otherwise).  Must be set before CUDA initialises.
-os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -67,6 +74,12 @@ def parse():
     ap.add_argument("--recompute", action="store_true",
                     help="activation recomputation (P:268-272); FLOPs then follow Eq. (2)'s 96-formula")
     ap.add_argument("--layers", type=int, default=0, help="override l (depth-reduced proxy; reported)")
+    ap.add_argument("--vocab", type=int, default=0,
+                    help="override V (e.g. 512: a negligible head, so the pipeline stages are balanced as the "
+                         "bubble formula assumes, P:104-118; reported in config)")
+    ap.add_argument("--bubble-batches", dest="bubble_batches", type=int, default=10,
+                    help="p > 1: extra batches run after the timed region with per-task events; the bubble "
+                         "is reported as the median over them (SURVEY 8(d): >= 10)")
     ap.add_argument("--B", type=int, default=16, help="global batch (sequences)")
     ap.add_argument("--b", type=int, default=2,
                     help="microbatch size (default 2: the best of the b in {1, 2, 4} sweep at 1.7B on 1xB200, "
@@ -194,7 +207,10 @@ def run_reference(args, cfg, world, rank):
     out = {"impl": "reference", "metric": METRIC, "value": val, "unit": "TFLOP/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic", "config": workload_config(args, cfg),
+           "data": "synthetic",
+           "config": dict(workload_config(args, cfg),
+                          workload=f"one unpartitioned GPT-{args.model}-width layer fwd+bwd, b=1, s={cfg.s}, "
+                                   f"fp64 numpy oracle on the host cores (a bounded sample of the iteration)"),
            "cpu_baseline": {"value": val, "unit": "TFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
            "e2e": {"value": val, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(out)
@@ -237,29 +253,45 @@ def replay_bubble(p, m, v, sched, tf, tb):
     return [(end[r] - busy[r]) / busy[r] for r in range(p)]
 
 
-def bubble_report(st, world, p, v, m, sched, d=1):
-    """Per-rank pipeline idle share of the last warm-up batch (max over ranks) next to
-    the closed form (p-1)/m or (p-1)/(v m), and the ideal-pipeline
-    estimate from this run's own per-task durations (equal stages assumed)."""
-    if not st:
+def bubble_report(stats_list, world, p, v, m, sched, d=1):
+    """Per-rank pipeline idle share (span_r - busy_r) / busy_r of each measured batch,
+    max over ranks, median over the batches, next to the closed form (p-1)/m or
+    (p-1)/(v m), and the ideal-pipeline replay of the library's own
+    static task orders with this run's measured per-stage task durations (zero
+    communication; captures stage imbalance such as the last stage's head)."""
+    stats_list = [st for st in stats_list if st]
+    if not stats_list:
         return None
     keys = ("bubble_measured", "pipeline_seconds", "busy_seconds", "t_fwd_task", "t_bwd_task", "iter_seconds")
-    vals = [st[k] for k in keys]
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
-        g = [torch.zeros_like(t) for _ in range(world)]
-        dist.all_gather(g, t)
-        per_rank = [x.tolist() for x in g]
-    else:
-        per_rank = [vals]
+    batches = []   # [batch][rank][key]
+    for st in stats_list:
+        vals = [st[k] for k in keys]
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+            g = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(g, t)
+            batches.append([x.tolist() for x in g])
+        else:
+            batches.append([vals])
+    per_batch = [max(r[0] for r in pr) for pr in batches]
+    med = float(np.median(per_batch))
+    mid = batches[int(np.argsort(per_batch)[len(per_batch) // 2])]
+    per_rank = [[float(np.median([pr[r][k] for pr in batches])) for k in range(len(keys))]
+                for r in range(len(batches[0]))]
+    st = stats_list[-1]
     rep = {"formula": st["bubble_formula"], "schedule": sched, "p": p, "v": v, "m": m,
-           "measured_max_over_ranks": max(r[0] for r in per_rank),
-           "measured_per_rank": [round(r[0], 5) for r in per_rank],
+           "batches": len(batches),
+           "measured_max_over_ranks": med,
+           "measured_max_over_ranks_per_batch": [round(x, 5) for x in per_batch],
+           "measured_per_rank_median_batch": [round(r[0], 5) for r in mid],
+           "rel_error_vs_formula": (med - st["bubble_formula"]) / st["bubble_formula"] if st["bubble_formula"] else None,
            "peak_inflight_rank0": st["peak_inflight"],
            "t_fwd_task_s": [round(r[3], 6) for r in per_rank], "t_bwd_task_s": [round(r[4], 6) for r in per_rank],
-           "flush_and_optimizer_s": max(r[5] - r[1] for r in per_rank)}
+           "flush_and_optimizer_s": max(r[5] - r[1] for r in per_rank),
+           "how": "per-task CUDA events on the compute stream; bubble_r = (last task end - batch start - "
+                  "sum of task durations) / sum of task durations; max over ranks, median over batches"}
     if p > 1:
         # pipeline stage r = the ranks with pp = r in replica 0, rank = (dp p + pp) t + tp
         # (TP ranks of a stage behave alike: use the max)
@@ -328,11 +360,16 @@ def workload_config(args, cfg):
 
 
 def main():
+    redirect_stdout()
+    # Enough hardware work queues that a stream's wait on a pipeline-channel flag
+    # (cuStreamWaitValue32, p2p.cu) never blocks unrelated streams' work through a
+    # shared queue.  Must be set before CUDA initialises (mp.py sets it too).
+    os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
     args = parse()
     import gen
     cfg = gen.CONFIGS[args.model]
-    if args.layers:
-        cfg = gen.ModelCfg(l=args.layers, h=cfg.h, a=cfg.a, s=cfg.s, V=cfg.V)
+    if args.layers or args.vocab:
+        cfg = gen.ModelCfg(l=args.layers or cfg.l, h=cfg.h, a=cfg.a, s=cfg.s, V=args.vocab or cfg.V)
     world, rank, local = dist_setup(args)
     if args.impl == "reference":
         run_reference(args, cfg, world, rank)
@@ -427,10 +464,16 @@ def main():
         torch.cuda.synchronize()
         w = (time.perf_counter() - w0) / args.steps
         w = launch.max_over_ranks(w, world, "cuda")
-        e2e = {"value": F / w / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": int(tok.nbytes),
+        e2e = {"value": F / w / 1e12 / world, "unit": "TFLOP/s (per GPU)", "h2d_bytes_per_step": int(tok.nbytes),
                "d2h_bytes_per_step": 4, "ms_per_step": 1e3 * w,
                "how": "mp_run_batch with pinned host tokens (H2D inside) and the loss read back every step; "
                       "wall clock with device sync, max over ranks"}
+    # ---- pipeline bubble over several batches (per-task CUDA events; outside the timed region)
+    bstats = []
+    if p > 1:
+        for _ in range(max(0, args.bubble_batches)):
+            bstats.append(ctx.run_batch_dev(B, b, m, sched, d_tok.data_ptr(), d_loss.data_ptr(),
+                                            apply_optimizer=True, stats=True))
     pk = peaks()
     agg = F / t_step / 1e12
     per_gpu = agg / world
@@ -443,15 +486,15 @@ def main():
         except Exception:
             traffic = None
     out = {
-        "metric": METRIC, "value": agg, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": per_gpu, "unit": "TFLOP/s per GPU", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform tokens, random-init weights)",
         "config": dict(workload_config(args, cfg), tp_comm=ctx.tp_comm_mode() if t > 1 else "none (t=1)"),
-        "per_gpu_tflops": per_gpu,
+        "per_gpu_tflops": per_gpu, "aggregate_tflops": agg,
         "pct_of_bf16_peak": {"measured_burst_1683": 100 * per_gpu / pk["bf16_burst"],
                              "measured_sustained": 100 * per_gpu / pk["bf16_sustained"],
                              "datasheet_2250": 100 * per_gpu / DATASHEET_BF16},
-        "model_flops_per_step": F, "eq2_96_formula_tflops_aggregate": F96 / t_step / 1e12,
+        "model_flops_per_step": F, "eq2_96_formula_tflops_per_gpu": F96 / t_step / 1e12 / world,
         "loss": loss_val,
         "roofline": {"kernel": "tcgen05 GEMM engine (all bf16 GEMM launches of the step)", "bound": "tensor",
                      "achieved": achieved, "peak": pk["bf16_sustained"], "unit": "TFLOP/s",
@@ -463,7 +506,7 @@ def main():
         "gpu_launches": int(launches),
         "step_ms_rank0": [round(x, 3) for x in step_ms],
         "clocks": clk,
-        "bubble": bubble_report(wstats, world, p, v, m, sched, d),
+        "bubble": bubble_report(bstats or [wstats], world, p, v, m, sched, d),
     }
     if world > 1:
         out["comm"] = comm_calibration(cfg, b, t, p, d, world, m, t_step)

@@ -8,8 +8,11 @@
  * under Megatron tensor parallelism (Sec. 2.3: column-parallel
  * QKV/FC1, row-parallel projection/FC2, conjugate f/g operators) composed with
  * the pipeline schedules of Sec. 2.2 (GPipe P:104-107, 1F1B P:109,
- * interleaved 1F1B P:112-120), with one process per GPU and NCCL for the
- * tensor-parallel all-reduces and pipeline point-to-point transfers.
+ * interleaved 1F1B P:112-120), with one process per GPU.  Tensor-parallel
+ * reductions use NCCL (ncclAllReduce) or, by default where the NVSwitch offers
+ * multicast, NVLS reduce-loads fused into the consuming kernels; pipeline
+ * point-to-point transfers use CUDA-IPC receive rings over NVLink written by
+ * the copy engine and flagged with stream memory operations (p2p.cu).
  *
  * Conventions
  *  - Every call returns an mp_status; no exceptions or exit() cross the ABI.
@@ -182,6 +185,20 @@ mp_status mp_layer_fwd(mp_ctx* ctx, int layer, int b, const void* x, void* y, in
  * stash slot is released.  Collective over the TP group. */
 mp_status mp_layer_bwd(mp_ctx* ctx, int layer, int b, int stash_slot, const void* dy, void* dx,
                        void* stream);
+
+/* The model head of the last pipeline stage (stage S-1, reading #12):
+ * Z = LN_f(x), logits = Z E_r^T over this rank's vocabulary shard (tied
+ * embedding, vocab-parallel over the TP group, readings #10-#11; the logit
+ * layer of Eq. (2)), token cross-entropy against `labels`, and its
+ * backward.  x, dx: device [s, b, h] in the storage dtype; labels: device
+ * int32, the label of position i of sequence j at labels[j * labels_ld + i]
+ * (labels_ld >= s; mp_run_batch passes tokens + 1 with labels_ld = s + 1).
+ * *loss_dev (device float) receives scale * sum of the b*s token losses;
+ * dx = d(that)/dx; scale * d/dE_r, d/dgamma_f, d/dbeta_f are ADDED to the fp32
+ * gradient accumulators.  MP_EINVAL on a rank that holds no head (pp != p-1).
+ * Collective over the TP group (max / sum-exp / target and dZ all-reduces). */
+mp_status mp_head_fwd_bwd(mp_ctx* ctx, int b, const void* x, const int* labels, int labels_ld, float scale,
+                          void* dx, float* loss_dev, void* stream);
 
 /* ------------------------------------------------------------- batch call */
 

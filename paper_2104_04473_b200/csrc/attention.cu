@@ -786,9 +786,14 @@ static const BwdWork* bwd_work(int zn, int nq, cudaStream_t st) {
   return ref.dev ? &ref : nullptr;
 }
 
+// D region padded to 32 floats so the dK / dV accumulators after it stay 128-byte aligned
+// (their float4 reduce-adds and loads need 16-byte alignment for any zn * s)
+static inline long long d_pad(long long n) { return (n + 31) & ~31LL; }
+
 long long flash_bwd_ws_floats(int s, int b, int heads, int hd) {
   // dQ accumulator, D, and (split mode) dK / dV accumulators
-  return (long long)b * heads * s * (3LL * hd + 1);
+  const long long zs = (long long)b * heads * s;
+  return 3LL * zs * hd + d_pad(zs);
 }
 
 // dQKV = d/dQKV of the fused attention, given O (= ctx), dO (= dctx), L2 from the forward.
@@ -808,7 +813,7 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
   if (!ok) return set_err(MP_ECUDA, "flash attention bwd: tensor map encode failed");
   float* dqacc = ws;
   float* D = ws + zn * s * hd;
-  float* dkacc = D + zn * s;
+  float* dkacc = D + d_pad(zn * s);
   float* dvacc = dkacc + zn * s * hd;
   const int nq = (s + 127) / 128;
   const BwdWork* work = bwd_work((int)zn, nq, st);

@@ -716,7 +716,7 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   }
   // CTA pairs (cta_group::2, 256 x BN tiles): halves each SM's B-operand traffic
   // from L2.  GEMMs with >= 2 row blocks, BN >= 128, TMA epilogue, and >= 60
-  // GFLOP: interleaved A/B timing (scratch/pair_ab.py, wg_ab.py) has the pair
+  // GFLOP: interleaved A/B timing (MP_GEMM_NO_PAIR on / off, round 1) had the pair
   // 3-23 % faster on the layer and logit GEMMs of >= 65 GFLOP and up to 14 %
   // slower on single-wave GEMMs below ~45 GFLOP.
   const bool no_pair = getenv("MP_GEMM_NO_PAIR") != nullptr;   // read per call (A/B timing)

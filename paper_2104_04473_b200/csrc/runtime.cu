@@ -5,10 +5,12 @@
 // static task order (schedule.h, identical to the oracle's) on one compute
 // stream.  Stage boundaries are crossed over four directed FIFO channels per
 // rank -- activations to the next device, activations from the previous one,
-// gradients to the previous device, gradients from the next one -- each a
-// 2-rank NCCL communicator with its own stream.  Every channel's send order
-// equals its receiver's consume order (checked by the oracle for every
-// schedule), so posting receives in this rank's consume order cannot
+// gradients to the previous device, gradients from the next one -- each with
+// its own stream (p2p.cu: CUDA-IPC receive rings in the peer's HBM, copy-engine
+// copies over NVLink, slot flags written / awaited with stream memory
+// operations, so no SM is held while a channel waits).  Every channel's send
+// order equals its receiver's consume order (checked by the oracle for every
+// schedule), so issuing receives in this rank's consume order cannot
 // deadlock and keeps the ideal bubble.  Compute waits on per-message events;
 // sends wait on the producing task's event.  After the flush the tied
 // embedding gradient is all-reduced between the first and last stage and
@@ -166,9 +168,10 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
     return set_err(MP_EINVAL, "dropout rates must be in [0, 1)");
   if (cfg->dtype != MP_BF16 && cfg->dtype != MP_FP32) return set_err(MP_EINVAL, "bad dtype");
   if (p > 1) {
-    // Six library streams (+ the caller's): fewer hardware queues create
-    // false dependencies between a compute-stream wait and a channel's NCCL
-    // kernel, which deadlocks the pipeline.
+    // Six library streams (+ the caller's): with fewer hardware queues a channel
+    // stream's cuStreamWaitValue32 on a peer's flag can sit in a queue shared
+    // with another stream's work and block it (a false dependency that can
+    // deadlock the pipeline).
     const char* mc = getenv("CUDA_DEVICE_MAX_CONNECTIONS");
     if (mc && atoi(mc) < 8)
       return set_err(MP_EINVAL, "CUDA_DEVICE_MAX_CONNECTIONS=%s is too small for p > 1 (need >= 8, use 32)", mc);
@@ -196,6 +199,14 @@ mp_status mp_init(int t, int p, int v, int d, const mp_model_cfg* cfg, int world
   MP_CUDA(cudaDeviceGetDefaultMemPool(&c->pool, local_device));
   uint64_t thr = UINT64_MAX;
   MP_CUDA(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  {
+    // Buffers freed on a pipeline-channel stream (which can block on a peer's flag) must never
+    // make the compute stream wait on that stream through a pool-inserted dependency: that
+    // would couple this rank's compute to the peer's progress (a possible cross-rank cycle).
+    // Event-ordered reuse stays on; internal dependencies are off.
+    int zero = 0;
+    cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseAllowInternalDependencies, &zero);
+  }
   if (getenv("MP_POOL_NOREUSE")) {
     int zero = 0;
     cudaMemPoolSetAttribute(c->pool, cudaMemPoolReuseFollowEventDependencies, &zero);
@@ -390,6 +401,23 @@ mp_status mp_layer_bwd(mp_ctx* c, int layer, int b, int slot, const void* dy, vo
   if (s == MP_OK) s = stash_release(c, it->second, c->cs);
   c->cs = saved;
   c->slots.erase(it);
+  return s;
+}
+
+mp_status mp_head_fwd_bwd(mp_ctx* c, int b, const void* x, const int* labels, int labels_ld, float scale, void* dx,
+                          float* loss_dev, void* stream) {
+  if (!c || !x || !labels || !dx || !loss_dev) return set_err(MP_EINVAL, "null argument");
+  if (!c->has_head) return set_err(MP_EINVAL, "rank %d (pp=%d) holds no head: only the last stage does", c->rank, c->pp);
+  if (b < 1 || labels_ld < c->cfg.s) return set_err(MP_EINVAL, "need b >= 1 and labels_ld >= s");
+  MP_CUDA(cudaSetDevice(c->device));
+  cudaStream_t saved = c->cs;
+  c->cs = reinterpret_cast<cudaStream_t>(stream);   // NULL = legacy default stream
+  mp_status s = MP_OK;
+  if (cudaMemsetAsync(c->d_loss, 0, 4, c->cs) != cudaSuccess) s = set_err(MP_ECUDA, "memset");
+  if (s == MP_OK) s = head_fwd_bwd(c, x, labels, labels_ld, b, scale, dx);
+  if (s == MP_OK && cudaMemcpyAsync(loss_dev, c->d_loss, 4, cudaMemcpyDeviceToDevice, c->cs) != cudaSuccess)
+    s = set_err(MP_ECUDA, "loss copy");
+  c->cs = saved;
   return s;
 }
 

@@ -12,9 +12,10 @@ import os
 import numpy as np
 
 # The pipeline runtime uses one compute stream, one side stream and four P2P
-# channel streams per process.  With fewer hardware work queues than streams,
-# a stream-wait on a P2P event can block a channel's NCCL kernel queued behind
-# it (false dependency -> deadlock), so ask for the maximum before CUDA
+# channel streams per process.  A channel stream waits on a peer's slot flag
+# with cuStreamWaitValue32 (p2p.cu); with fewer hardware work queues than
+# streams that wait can sit in a queue shared with another stream's work and
+# block it (false dependency -> deadlock), so ask for the maximum before CUDA
 # initialises in this process.  mp_init refuses p > 1 when the setting is
 # too small.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
@@ -88,6 +89,7 @@ SIGNATURES = {
     "mp_zero_grads": (_I, [_P]),
     "mp_layer_fwd": (_I, [_P, _I, _I, _P, _P, ctypes.POINTER(_I), _P]),
     "mp_layer_bwd": (_I, [_P, _I, _I, _I, _P, _P, _P]),
+    "mp_head_fwd_bwd": (_I, [_P, _I, _P, _P, _I, _F, _P, _P, _P]),
     "mp_run_batch": (_I, [_P, _I, _I, _I, _I, _P, _I, ctypes.POINTER(_F), ctypes.POINTER(BatchStats)]),
     "mp_compute_stream": (_P, [_P]),
     "mp_tp_comm_mode": (_I, [_P]),
@@ -258,6 +260,10 @@ class Context:
 
     def layer_bwd(self, layer, b, slot, dy_ptr, dx_ptr, stream=0):
         _check(_sym("mp_layer_bwd")(self.ptr, layer, b, slot, dy_ptr, dx_ptr, stream))
+
+    def head_fwd_bwd(self, b, x_ptr, labels_ptr, labels_ld, scale, dx_ptr, loss_ptr, stream=0):
+        """Last-stage head (final LN, tied logits, cross-entropy) fwd + bwd; device addresses."""
+        _check(_sym("mp_head_fwd_bwd")(self.ptr, b, x_ptr, labels_ptr, labels_ld, scale, dx_ptr, loss_ptr, stream))
 
     def run_batch(self, B, b, m, sched, tokens, apply_optimizer=False, stats=True):
         """tokens: numpy int32 [B, s+1] or an integer host address (e.g. pinned memory)."""

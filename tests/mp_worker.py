@@ -11,9 +11,10 @@ import sys
 
 import numpy as np
 
-# Enough hardware work queues that the compute stream's waits on P2P events
-# never sit in front of a channel stream's NCCL kernel (false dependencies
-# deadlock the pipeline otherwise).  Must be set before CUDA initialises.
+# Enough hardware work queues that a channel stream's wait on a peer's slot
+# flag (cuStreamWaitValue32, p2p.cu) never blocks another stream's work through
+# a shared queue (false dependencies deadlock the pipeline otherwise).  Must be
+# set before CUDA initialises.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -35,6 +36,9 @@ def main():
     ap.add_argument("--tpcomm", default="auto")
     ap.add_argument("--dp", dest="d", type=int, default=1)
     ap.add_argument("--recompute", type=int, default=0)
+    ap.add_argument("--a", dest="heads", type=int, default=4)
+    ap.add_argument("--s", type=int, default=0, help="sequence length (default 32 unfused / 64 fused)")
+    ap.add_argument("--V", type=int, default=512)
     ap.add_argument("--out", default="")
     # arguments come through MP_WORKER_ARGS: torchrun's own parser would
     # otherwise claim any option that prefixes one of its flags (--m, --t ...)
@@ -52,7 +56,7 @@ def main():
     dist.init_process_group("gloo", init_method="env://")
     nid = [mp.mp_nccl_get_id() if rank == 0 else None]
     dist.broadcast_object_list(nid, src=0)
-    shape = gen.ModelCfg(l=a.l, h=a.h, a=4, s=32 if a.attn == "unfused" else 64, V=512)
+    shape = gen.ModelCfg(l=a.l, h=a.h, a=a.heads, s=a.s or (32 if a.attn == "unfused" else 64), V=a.V)
     W = gen.model_weights(shape, seed=42, dtype=a.dtype)
     tok = gen.tokens(a.m * a.d, shape.s, shape.V, seed=1234)   # the global batch; replica dp takes its rows
     cfg = mp.make_cfg(shape.l, shape.h, shape.a, shape.s, shape.V, dtype=a.dtype, attn=a.attn,
@@ -74,8 +78,21 @@ def main():
             from oracle import philox as PH
             masks = [[PH.layer_masks(4321, k, [i], shape.s, shape.h, shape.a, a.pdrop, a.pdrop)
                       for k in range(shape.l)] for i in range(a.m * a.d)]
-        # the oracle runs the whole global batch in one process: d replicas x m microbatches
-        lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m * a.d, masks=masks)
+        # the oracle runs the whole global batch in one process: d replicas x m microbatches;
+        # at paper widths rank 0 computes it once and the other ranks read its result
+        if a.out and shape.h >= 1024:
+            import pickle
+            path = a.out + ".oracle.pkl"
+            if rank == 0:
+                res = M.batch_fwd_bwd(W, tok, shape.a, a.m * a.d, masks=masks)
+                with open(path + ".tmp", "wb") as f:
+                    pickle.dump(res, f)
+                os.replace(path + ".tmp", path)
+            dist.barrier()
+            with open(path, "rb") as f:
+                lr, gr = pickle.load(f)
+        else:
+            lr, gr = M.batch_fwd_bwd(W, tok, shape.a, a.m * a.d, masks=masks)
         report["loss"] = [loss, lr]
         report["stats"] = stats
         report["tp_comm"] = ctx.tp_comm_mode()

@@ -201,3 +201,27 @@ def test_multi_gpu_recompute(tmp_path, t, p, v, m, sched, attn, pdrop):
     h = 128 if attn == "fused" else 64
     _run_worker(tmp_path, n, f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype bf16 --h {h} "
                 f"--l {max(4, p * v)} --attn {attn} --pdrop {pdrop} --recompute 1", 41000, (t, p, v, m, sched, attn))
+
+
+@pytest.mark.parametrize("t,p,v,m,sched", [(2, 2, 2, 2, "interleaved"), (4, 1, 1, 2, "1f1b"), (1, 4, 1, 4, "1f1b")])
+def test_multi_gpu_paper_width(tmp_path, t, p, v, m, sched):
+    """Paper-width model on 4 GPUs (SURVEY 8(c) tier 3; VERDICT r01 next-round
+    item 1c): h=2304, a=24, s=2048, V=51200 (the 1.7B config's width and the
+    paper's vocabulary, P:342), l = 4, fused attention, bf16; every rank's
+    shards of every gradient and the loss vs the fp64 oracle (computed once by
+    rank 0)."""
+    n = t * p
+    if ngpus() < n:
+        pytest.skip(f"needs {n} GPUs")
+    out = str(tmp_path / "rep")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}",
+           os.path.join(ROOT, "tests", "mp_worker.py")]
+    env = dict(os.environ, MP_WORKER_ARGS=f"--tp {t} --pp {p} --vp {v} --m {m} --sched {sched} --dtype bf16 "
+                                          f"--h 2304 --a 24 --s 2048 --V 51200 --l 4 --attn fused --out {out}")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT, env=env)
+    reps = [json.load(open(f)) for f in sorted(glob.glob(out + ".*.json"))]
+    msg = r.stdout[-3000:] + r.stderr[-3000:] + json.dumps(reps)[:4000]
+    assert r.returncode == 0, msg
+    assert len(reps) == n and all(x["ok"] for x in reps), msg
+    assert len({round(x["loss"][0], 5) for x in reps}) == 1, msg
