@@ -87,7 +87,7 @@ long long mp_launch_count(void);
 
 /* LayerNorm over rows of x [R, h] (implied by Eq. (1)'s 13h term, P:344;
  * pre-LN GPT layer, reading #1; biased variance, eps): y = g * xhat + b;
- * per-row fp32 mean / rstd saved for the backward.  h <= 8192 (bf16). */
+ * per-row fp32 mean / rstd saved for the backward.  h <= 16384 (bf16), 8192 (fp32). */
 mp_status mp_op_layernorm_fwd(mp_dtype dt, const void* x, const void* g, const void* b, void* y, float* mean,
                               float* rstd, int R, int h, float eps, void* stream);
 
@@ -97,12 +97,23 @@ mp_status mp_op_bda_layernorm_fwd(mp_dtype dt, const void* y, const void* bias, 
                                   const void* g, const void* b, void* out, float* mean, float* rstd, int R, int h,
                                   float eps, void* stream);
 
-/* LayerNorm backward: dx = LN'(dy) (+ dres if non-NULL); dgamma, dbeta
- * (fp32 [h]) are ACCUMULATED (+=).  scratch is unused (may be NULL);
- * mp_op_layernorm_bwd_scratch_floats returns 0 and is kept for ABI stability. */
+/* LayerNorm backward (a17; P:574 counts it with the layer): dx = LN'(dy)
+ * (+ dres if non-NULL); dgamma, dbeta (fp32 [h]) are ACCUMULATED (+=).
+ * One pass over the rows; every CTA writes its column partials to `scratch`
+ * (device fp32, caller-owned, mp_op_layernorm_bwd_scratch_floats(R, h)
+ * floats; 0 without a device) and a second kernel adds their sums into the
+ * accumulators in a fixed order.  MP_EINVAL if scratch is NULL. */
 mp_status mp_op_layernorm_bwd(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
                               const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
                               float* scratch, int R, int h, void* stream);
+/* Same, also accumulating the column sums of dres (dres_sum) and of the
+ * stored dx (dx_sum), either may be NULL, both need dres: in the layer
+ * backward around LN2 these are the bias gradients of FC2 (b2: column sum of
+ * the layer's output gradient, P:146 bias added after g) and of the
+ * projection (bo: column sum of dX1), so no separate column-sum pass runs. */
+mp_status mp_op_layernorm_bwd_sums(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
+                                   const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
+                                   float* dres_sum, float* dx_sum, float* scratch, int R, int h, void* stream);
 long long mp_op_layernorm_bwd_scratch_floats(int R, int h);
 
 /* Fused bias + tanh-GeLU (reading #3): out = gelu(y + b), y [R, N]. */

@@ -28,6 +28,7 @@
 #include "ptx.cuh"
 #include "common.h"
 #include "tma_host.h"
+#include "gemm.h"
 #include "../../include/mp_ops.h"
 
 namespace mp {
@@ -67,6 +68,14 @@ struct TcArgs {
   int pair;             // CTA-pair kernel: m_blocks count 256-row pair tiles
   int kb_per_tile;      // k-blocks per tile (stream_k)
   float alpha;
+  // act 3 (logit layer + cross-entropy statistics, a18 / P:577): besides the bf16
+  // logits, per (row, n-block, epilogue half) the fp32 max and sum of exp(x - max)
+  // of the unrounded logits -> ce_part[row][2 n_blocks] (float2), and the fp32
+  // target logit of rows whose label falls in this shard -> ce_tgt[row]
+  float2* ce_part;
+  float* ce_tgt;
+  const int* ce_lab;    // labels, row r = i*b + beta -> ce_lab[beta * ce_lab_ld + i] - ce_v0
+  int ce_lab_ld, ce_b, ce_v0;
 };
 
 __device__ __forceinline__ bool tile_skipped(const TcArgs& g, int m_blk, int n_blk, int BN) {
@@ -142,7 +151,7 @@ struct WorkIter {
   }
 };
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR>
+template <int BN, bool A_MN, bool B_MN, bool PAIR, bool CE = false>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
 tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmC2, TcArgs g) {
@@ -300,6 +309,12 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       tc_fence_after();
       const int row0 = m_blk * (PAIR ? 2 * BM : BM) + (int)rank * BM + quarter * 32;
       const uint32_t tbase = tmem_base + acc * BN + ((uint32_t)(quarter * 32) << 16);
+      float ce_m = -INFINITY, ce_s = 0.f;   // CE: this lane's row over this warp's column boxes
+      int ce_t = -1;                        // CE: label column relative to the tile, if in the tile
+      if (CE && row0 + lane < g.M) {
+        const int r = row0 + lane;
+        ce_t = g.ce_lab[(long long)(r % g.ce_b) * g.ce_lab_ld + r / g.ce_b] - g.ce_v0 - n_blk * BN;
+      }
       if (g.tma_out) {
         // TMEM -> registers -> 128B-swizzled staging box (32 rows x 128 B) -> TMA
         // store (bf16 / fp32) or TMA reduce-add (fp32 gradient accumulation).
@@ -363,6 +378,25 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 const int gc = col0 + 32 * hf + c;
                 if (g.bias && gc < g.N) a0 += __bfloat162float(g.bias[gc]);
                 x[32 * hf + c] = a0;
+              }
+            }
+            if constexpr (CE) {
+              // cross-entropy statistics of the unrounded logits (columns >= N excluded; the TMA
+              // store clips them anyway) and the target logit, online over this warp's boxes
+              float bm = -INFINITY;
+#pragma unroll
+              for (int e = 0; e < 64; ++e) {
+                if (col0 + e >= g.N) x[e] = -INFINITY;
+                bm = fmaxf(bm, x[e]);
+                if (ce_t == c0 + e) g.ce_tgt[row0 + lane] = x[e];
+              }
+              if (bm > -INFINITY) {
+                const float mn = fmaxf(ce_m, bm);
+                float s = 0.f;
+#pragma unroll
+                for (int e = 0; e < 64; ++e) s += exp2f((x[e] - mn) * 1.4426950408889634f);
+                ce_s = ce_s * exp2f((ce_m - mn) * 1.4426950408889634f) + s;
+                ce_m = mn;
               }
             }
             if (g.act == 2) {
@@ -458,6 +492,8 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             bulk_commit();
           }
         }
+        if (CE && row0 + lane < g.M)
+          g.ce_part[(long long)(row0 + lane) * (2 * g.n_blocks) + 2 * n_blk + half] = make_float2(ce_m, ce_s);
       } else {
         const int row = row0 + lane;
         const bool row_ok = row < g.M;
@@ -607,11 +643,11 @@ static int pick_bn(const mp_gemm_desc& g) {
   return 256;
 }
 
-template <int BN, bool A_MN, bool B_MN, bool PAIR>
+template <int BN, bool A_MN, bool B_MN, bool PAIR, bool CE = false>
 static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
                              const CUtensorMap& tc2, const TcArgs& a, int grid, cudaStream_t st) {
   using Cfg = TcCfg<BN, PAIR>;
-  auto k = tc_gemm_kernel<BN, A_MN, B_MN, PAIR>;
+  auto k = tc_gemm_kernel<BN, A_MN, B_MN, PAIR, CE>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
@@ -669,7 +705,7 @@ static bool want_stream_k(const TcArgs& a) {
   return fill < 0.9 && iters / G >= 8;
 }
 
-mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
+mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st, const GemmCe* ce = nullptr) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return set_err(MP_EINVAL, "gemm: empty shape");
   if (g.accumulate && !g.c_fp32) return set_err(MP_EINVAL, "gemm: accumulate needs fp32 C");
   auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -697,6 +733,17 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   a.act = g.act;
   a.aux = reinterpret_cast<const __nv_bfloat16*>(g.C2);
   a.colsum = g.colsum;
+  a.ce_part = nullptr; a.ce_tgt = nullptr; a.ce_lab = nullptr;
+  a.ce_lab_ld = 0; a.ce_b = 1; a.ce_v0 = 0;
+  if (ce) {
+    if (g.act || g.c_fp32 || g.accumulate || g.bias || g.causal || g.batch != 1 || !a.tma_out)
+      return set_err(MP_EINVAL, "gemm: the cross-entropy epilogue needs a plain bf16 GEMM (16-byte aligned C)");
+    a.act = 3;
+    a.ce_part = ce->part; a.ce_tgt = ce->tgt; a.ce_lab = ce->lab;
+    a.ce_lab_ld = ce->lab_ld; a.ce_b = ce->b; a.ce_v0 = ce->v0;
+  } else if (g.act == 3) {
+    return set_err(MP_EINVAL, "gemm: act 3 is internal (logit layer)");
+  }
   if (g.act == 2) {
     if (g.c_fp32 || g.accumulate || g.bias || !a.tma_out || !g.C2 || g.causal)
       return set_err(MP_EINVAL, "gemm: act 2 needs bf16 C, the pre-activation C2, no bias / accumulate");
@@ -737,7 +784,14 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st) {
   if (!ok) return set_err(MP_ECUDA, "gemm: cuTensorMapEncodeTiled failed");
   const int grid = tc_grid(a);
   cudaError_t e;
-  if (a.pair) {
+  if (a.act == 3) {   // logit GEMM (both operands K-major) with the cross-entropy statistics epilogue
+    if (g.a_major || g.b_major) return set_err(MP_EINVAL, "gemm: CE epilogue needs K-major operands");
+    if (a.pair) e = BN == 128 ? launch_tc<128, false, false, true, true>(ta, tb, tc, tc2, a, grid, st)
+                              : launch_tc<256, false, false, true, true>(ta, tb, tc, tc2, a, grid, st);
+    else if (BN == 64) e = launch_tc<64, false, false, false, true>(ta, tb, tc, tc2, a, grid, st);
+    else if (BN == 128) e = launch_tc<128, false, false, false, true>(ta, tb, tc, tc2, a, grid, st);
+    else e = launch_tc<256, false, false, false, true>(ta, tb, tc, tc2, a, grid, st);
+  } else if (a.pair) {
     if (BN == 128) e = dispatch_major<128, true>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
     else e = dispatch_major<256, true>(ta, tb, tc, tc2, a, grid, g.a_major, g.b_major, st);
   } else {
@@ -774,6 +828,13 @@ double gemm_algorithmic_flops(const mp_gemm_desc& g) {
   return 2.0 * rows * (g.causal == 1 ? g.K : g.N) * g.batch;
 }
 
+// Logit GEMM with the cross-entropy statistics epilogue (act 3): n-blocks of the
+// launch, so the caller can size ce_part ([M][2 n_blocks] float2).
+int gemm_ce_nblocks(const mp_gemm_desc& g) {
+  const int BN = pick_bn(g);
+  return (g.N + BN - 1) / BN;
+}
+
 struct ProfRec { cudaEvent_t a, b; double flops; };
 static bool g_prof = false;
 static std::vector<ProfRec> g_recs;
@@ -788,13 +849,13 @@ static cudaEvent_t prof_event() {
   return g_evpool[g_evnext++];
 }
 
-mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st) {
-  if (dt != MP_BF16) { count_launch(); return gemm_fp32(g, st); }
+mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st, const GemmCe* ce) {
+  if (dt != MP_BF16) { count_launch(); return ce ? set_err(MP_EINVAL, "gemm: CE epilogue is bf16") : gemm_fp32(g, st); }
   count_launch();
-  if (!g_prof) return gemm_bf16(g, st);
+  if (!g_prof) return gemm_bf16(g, st, ce);
   ProfRec r{prof_event(), prof_event(), gemm_algorithmic_flops(g)};
   cudaEventRecord(r.a, st);
-  mp_status s = gemm_bf16(g, st);
+  mp_status s = gemm_bf16(g, st, ce);
   cudaEventRecord(r.b, st);
   g_recs.push_back(r);
   return s;

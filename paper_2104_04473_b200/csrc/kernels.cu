@@ -105,20 +105,6 @@ __device__ __forceinline__ uint32_t keep_bits(const Dropout& d, unsigned long lo
   return m;
 }
 
-static int row_threads(int nvec) {
-  int t = ((nvec + 3) / 4 + 31) / 32 * 32;   // <= 4 vectors per thread
-  return std::max(32, std::min(256, t));
-}
-constexpr int LN_MAXV = 4;
-// Grid of a row kernel: every row handled by one CTA in a grid-stride loop, the grid
-// sized to the CTAs that are resident at once (<= 64 warps / 32 CTAs per SM), so there
-// is no partial last wave (T = 4096 rows of 96 threads would be 1.3 waves).
-static int row_grid(long long R, int nvec) {
-  const int warps = row_threads(nvec) / 32;
-  const int per_sm = std::max(1, std::min(32, 64 / warps));
-  return (int)std::max(1LL, std::min<long long>(R, (long long)num_sms() * per_sm));
-}
-
 #define LAUNCH_CHECK()                                                                         \
   do {                                                                                         \
     count_launch();                                                                            \
@@ -127,103 +113,183 @@ static int row_grid(long long R, int nvec) {
     return MP_OK;                                                                              \
   } while (0)
 
-// ------------------------------------------------------------ LayerNorm fwd
-// mode 0: x = in; mode 1: x = r + yv + bias (bias-dropout-add with p = 0), x1 <- x.
-template <class T, int MODE, bool RED = false>
-__global__ void __launch_bounds__(256) ln_fwd_kernel(const T* __restrict__ in, const T* __restrict__ bias,
-                                                     const T* __restrict__ res, T* __restrict__ x1,
-                                                     const T* __restrict__ g, const T* __restrict__ b,
-                                                     T* __restrict__ out, float* __restrict__ mean,
-                                                     float* __restrict__ rstd, int h, float eps, Dropout dp, int R) {
+// ------------------------------------------------------------ LayerNorm
+// Row-group layout shared by the LayerNorm kernels (coalesced,
+// warp-shuffle rows).  A row of h elements (nvec 16-byte vectors) belongs to a
+// group of RG threads (a multiple of 32); thread lt of the group holds vectors
+// lt + k RG (k < NV) in registers.  A CTA runs NG groups on different rows and
+// is persistent (grid = resident CTAs, rows visited in a grid-stride loop), so
+// a thread owns the same columns for every row it visits -- the backward keeps
+// its dgamma / dbeta / bias-gradient column partials in registers across rows.
+// Per-row sums: warp shuffles, then one shared-memory exchange under the
+// group's named barrier (double-buffered, so one barrier per reduction).
+struct RowCfg { int nvec, NV, RG, NG; };
+constexpr int ROW_THREADS = 256;                   // CTA size bound (<= 255 registers per thread)
+constexpr int ROW_MAX_NG = 8, ROW_MAX_WARPS = 8;   // named barriers 1..8; RG <= 256
+
+// NV in {1, 2, 3, 4, 8} with RG = roundup32(ceil(nvec / NV)) <= 256 and the fewest idle
+// lanes (h = 2304 bf16: NV = 3, RG = 96; h = 4096: 2 x 256; h = 8192: 4 x 256).
+template <class T>
+static RowCfg row_cfg(int h) {
   constexpr int V = VW<T>::N;
-  __shared__ float2 red[32];
-  const int nvec = h / V;
-  // grid-stride over rows: a grid of a few resident CTAs per SM, no partial last wave
-  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
-  float v[LN_MAXV][V];
-  float s1 = 0.f;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      ld_in<RED>(in + row * h + vi * V, v[k]);
-      if (MODE == 1) {
-        float bb[V], rr[V];
-        ld_vec(bias + vi * V, bb);
-        ld_vec(res + row * h + vi * V, rr);
-        if (dp.on()) {   // x1 = r + dropout(y + bias), mask keyed by (sequence, position, feature)
-          const int pos = (int)(row / dp.b), seq = dp.seq0 + (int)(row % dp.b);
-          const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * h + vi * V, 0, seq);
-#pragma unroll
-          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + ((km >> e) & 1 ? (v[k][e] + bb[e]) * dp.scale : 0.f);
-        } else {
-#pragma unroll
-          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
-        }
-        st_vec(x1 + row * h + vi * V, v[k]);
-        // LayerNorm consumes the stored (rounded) residual stream value
-        ld_vec(x1 + row * h + vi * V, v[k]);
-      }
-#pragma unroll
-      for (int e = 0; e < V; ++e) s1 += v[k][e];
-    }
+  RowCfg r;
+  r.nvec = h / V;
+  r.NV = 8;
+  r.RG = ROW_THREADS;
+  long long best = -1;
+  for (int nv : {1, 2, 3, 4, 8}) {
+    const int rg = ((r.nvec + nv - 1) / nv + 31) / 32 * 32;
+    if (rg > ROW_THREADS) continue;
+    const long long waste = (long long)rg * nv - r.nvec;
+    if (best < 0 || waste < best) { best = waste; r.NV = nv; r.RG = rg; }
   }
-  const float mu = block_sum2(s1, 0.f, red).x / h;
-  float s2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec)
-#pragma unroll
-      for (int e = 0; e < V; ++e) { float d = v[k][e] - mu; s2 += d * d; }
-  }
-  const float var = block_sum2(s2, 0.f, red).x / h;
-  const float rs = rsqrtf(var + eps);
-#pragma unroll
-  for (int k = 0; k < LN_MAXV; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      float gg[V], bb[V], o[V];
-      ld_vec(g + vi * V, gg);
-      ld_vec(b + vi * V, bb);
-#pragma unroll
-      for (int e = 0; e < V; ++e) o[e] = (v[k][e] - mu) * rs * gg[e] + bb[e];
-      st_vec(out + row * h + vi * V, o);
-    }
-  }
-  if (threadIdx.x == 0) { mean[row] = mu; rstd[row] = rs; }
-  }
+  r.NG = std::max(1, std::min(ROW_MAX_NG, ROW_THREADS / r.RG));
+  return r;
 }
 
 template <class T>
 static mp_status check_row_dims(int R, int h) {
   constexpr int V = VW<T>::N;
   if (R <= 0 || h <= 0 || h % V) return set_err(MP_EINVAL, "row kernel: h=%d must be a multiple of %d", h, V);
-  if (h / V > LN_MAXV * 256) return set_err(MP_EINVAL, "row kernel: h=%d too large", h);
+  if (h / V > 8 * ROW_THREADS) return set_err(MP_EINVAL, "row kernel: h=%d too large", h);
   return MP_OK;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// (a, b) summed over the RG threads of the caller's row group; red holds
+// RG / 32 float2 of this group and is not reused before the group's next
+// barrier (callers alternate two buffers).
+__device__ __forceinline__ float2 group_sum2(float a, float b, float2* red, int lt, int RG, int bar) {
+  a = warp_sum(a);
+  b = warp_sum(b);
+  if (RG == 32) return make_float2(a, b);
+  if ((lt & 31) == 0) red[lt >> 5] = make_float2(a, b);
+  named_bar(bar, RG);
+  float2 r = make_float2(0.f, 0.f);
+  for (int i = 0; i < RG / 32; ++i) { r.x += red[i].x; r.y += red[i].y; }
+  return r;
+}
+// values as stored in T (bf16 rounding of an fp32 result, identity for fp32)
+template <class T, int V>
+__device__ __forceinline__ void round_as(float (&o)[V]) {
+  if constexpr (sizeof(T) == 2) {
+#pragma unroll
+    for (int e = 0; e < V; ++e) o[e] = __bfloat162float(__float2bfloat16_rn(o[e]));
+  }
+}
+
+template <class K>
+static int resident_ctas(K kernel, int threads, size_t smem) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    n = 1;
+  }
+  return std::max(1, n);
+}
+
+// mode 0: x = in; mode 1: x1 = r + dropout(in + bias) is stored and x = x1 as stored.
+template <class T, int NV, int MODE, bool RED>
+__global__ void __launch_bounds__(ROW_THREADS) ln_fwd_kernel(const T* __restrict__ in, const T* __restrict__ bias,
+                                                      const T* __restrict__ res, T* __restrict__ x1,
+                                                      const T* __restrict__ g, const T* __restrict__ b,
+                                                      T* __restrict__ out, float* __restrict__ mean,
+                                                      float* __restrict__ rstd, int h, float eps, Dropout dp, int R,
+                                                      int RG, int NG) {
+  constexpr int V = VW<T>::N;
+  __shared__ float2 red[2][ROW_MAX_NG][ROW_MAX_WARPS];
+  const int grp = threadIdx.x / RG, lt = threadIdx.x - grp * RG;
+  const int nvec = h / V;
+  for (long long row = (long long)blockIdx.x * NG + grp; row < R; row += (long long)gridDim.x * NG) {
+    float v[NV][V];
+    float s1 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = lt + k * RG;
+      if (vi < nvec) {
+        ld_in<RED>(in + row * h + vi * V, v[k]);
+        if constexpr (MODE == 1) {
+          float bb[V], rr[V];
+          ld_vec(bias + vi * V, bb);
+          ld_vec(res + row * h + vi * V, rr);
+          if (dp.on()) {   // x1 = r + dropout(y + bias), mask keyed by (sequence, position, feature)
+            const int pos = (int)(row / dp.b), seq = dp.seq0 + (int)(row % dp.b);
+            const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * h + vi * V, 0, seq);
+#pragma unroll
+            for (int e = 0; e < V; ++e) v[k][e] = rr[e] + ((km >> e) & 1 ? (v[k][e] + bb[e]) * dp.scale : 0.f);
+          } else {
+#pragma unroll
+            for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
+          }
+          st_vec(x1 + row * h + vi * V, v[k]);
+          round_as<T>(v[k]);   // LayerNorm consumes the stored residual-stream value
+        }
+#pragma unroll
+        for (int e = 0; e < V; ++e) s1 += v[k][e];
+      }
+    }
+    const float mu = group_sum2(s1, 0.f, red[0][grp], lt, RG, 1 + grp).x / h;
+    float s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = lt + k * RG;
+      if (vi < nvec)
+#pragma unroll
+        for (int e = 0; e < V; ++e) { const float d = v[k][e] - mu; s2 += d * d; }
+    }
+    const float var = group_sum2(s2, 0.f, red[1][grp], lt, RG, 1 + grp).x / h;
+    const float rs = rsqrtf(var + eps);
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = lt + k * RG;
+      if (vi < nvec) {
+        float gg[V], bb[V], o[V];
+        ld_vec(g + vi * V, gg);
+        ld_vec(b + vi * V, bb);
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] = (v[k][e] - mu) * rs * gg[e] + bb[e];
+        st_vec(out + row * h + vi * V, o);
+      }
+    }
+    if (lt == 0) { mean[row] = mu; rstd[row] = rs; }
+  }
+}
+
+template <class T, int MODE, bool RED>
+static mp_status launch_ln_fwd(const T* in, const T* bias, const T* res, T* x1, const T* g, const T* b, T* out,
+                               float* mean, float* rstd, int R, int h, float eps, Dropout dp, cudaStream_t st) {
+  MP_TRY(check_row_dims<T>(R, h));
+  const RowCfg rc = row_cfg<T>(h);
+  auto go = [&](auto kern) {
+    const int threads = rc.RG * rc.NG;
+    const long long need = (R + rc.NG - 1) / rc.NG;
+    const int grid = (int)std::min<long long>(need, (long long)num_sms() * resident_ctas(kern, threads, 0));
+    kern<<<grid, threads, 0, st>>>(in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R, rc.RG, rc.NG);
+  };
+  switch (rc.NV) {
+    case 1: go(ln_fwd_kernel<T, 1, MODE, RED>); break;
+    case 2: go(ln_fwd_kernel<T, 2, MODE, RED>); break;
+    case 3: go(ln_fwd_kernel<T, 3, MODE, RED>); break;
+    case 4: go(ln_fwd_kernel<T, 4, MODE, RED>); break;
+    default: go(ln_fwd_kernel<T, 8, MODE, RED>); break;
+  }
+  LAUNCH_CHECK();
 }
 
 template <class T>
 mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int R, int h, float eps,
                         cudaStream_t st) {
-  MP_TRY(check_row_dims<T>(R, h));
-  ln_fwd_kernel<T, 0><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(
-      x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, h, eps, Dropout{}, R);
-  LAUNCH_CHECK();
+  return launch_ln_fwd<T, 0, false>(x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, R, h, eps, Dropout{}, st);
 }
 
 template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
                             float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp,
                             bool red) {
-  MP_TRY(check_row_dims<T>(R, h));
-  if (red)
-    ln_fwd_kernel<T, 1, true><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(
-        yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp, R);
-  else
-    ln_fwd_kernel<T, 1><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(
-        yv, bias, r, x1, g, b, out, mean, rstd, h, eps, dp, R);
-  LAUNCH_CHECK();
+  if (red) return launch_ln_fwd<T, 1, true>(yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
+  return launch_ln_fwd<T, 1, false>(yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
 }
 
 // ------------------------------------------------------ bias + residual add
@@ -270,59 +336,154 @@ mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long
 }
 
 // ------------------------------------------------------------ LayerNorm bwd
-// dx: one CTA per row (fp32 block sums of dxhat and dxhat*xhat).
+// One pass over the rows (a17): dx = rs (g dy - mean(g dy) - xhat mean(g dy xhat))
+// (+ dres), and the column sums dgamma = sum dy xhat, dbeta = sum dy, and with
+// SUMS also sum dres and sum dx (of the stored dx): the bias gradients of the
+// layer's two row-parallel outputs (b2 = colsum of the layer output gradient,
+// the residual input here; bo = colsum of dX1, the output here).  Each thread
+// keeps its columns' partials in registers over the CTA's rows; the NG groups
+// combine them in shared memory and the CTA writes one row of partials
+// part[blockIdx.x][NACC][h]; ln_part_reduce_kernel adds the column sums of part
+// into the fp32 accumulators (no global atomics, fixed summation order).
 // RED: dy is a multicast address (NVLS reduce-load of the TP partial sums); the
-// reduced rows are also stored to dy_copy for the gamma/beta kernel.
-template <class T, bool RED = false>
-__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                        const T* __restrict__ g, const float* __restrict__ mean,
-                                                        const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy, int R) {
+// reduced rows are also stored to dy_copy.
+template <class T, int NV, bool RED, bool DRES, bool SUMS>
+__global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                      const T* __restrict__ g, const float* __restrict__ mean,
+                                                      const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                      T* __restrict__ dx, T* __restrict__ dy_copy,
+                                                      float* __restrict__ part, int h, int R, int RG, int NG) {
   constexpr int V = VW<T>::N;
-  __shared__ float2 red[32];
+  constexpr int NACC = SUMS ? 4 : 2;
+  extern __shared__ float sacc[];   // [NACC][h]
+  __shared__ float2 red[2][ROW_MAX_NG][ROW_MAX_WARPS];
+  const int grp = threadIdx.x / RG, lt = threadIdx.x - grp * RG;
   const int nvec = h / V;
-  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
-  const float mu = mean[row], rs = rstd[row];
-  float xh[LN_MAXV][V], dxh[LN_MAXV][V];
-  float s1 = 0.f, s2 = 0.f;
+  if (NG > 1) {
+    for (int j = threadIdx.x; j < NACC * h; j += blockDim.x) sacc[j] = 0.f;
+    __syncthreads();
+  }
+  float ag[NV][V], ab[NV][V], ar[NV][V], ax[NV][V];
 #pragma unroll
-  for (int k = 0; k < LN_MAXV; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      float d[V], xv[V], gg[V];
-      ld_in<RED>(dy + row * h + vi * V, d);
-      if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
-      ld_vec(x + row * h + vi * V, xv);
-      ld_vec(g + vi * V, gg);
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int e = 0; e < V; ++e) { ag[k][e] = 0.f; ab[k][e] = 0.f; ar[k][e] = 0.f; ax[k][e] = 0.f; }
+  int par = 0;
+  for (long long row = (long long)blockIdx.x * NG + grp; row < R; row += (long long)gridDim.x * NG) {
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NV][V], dxh[NV][V];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = lt + k * RG;
+      if (vi < nvec) {
+        float d[V], xv[V], gg[V];
+        ld_in<RED>(dy + row * h + vi * V, d);
+        if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
+        ld_vec(x + row * h + vi * V, xv);
+        ld_vec(g + vi * V, gg);
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          xh[k][e] = (xv[e] - mu) * rs;
+          dxh[k][e] = d[e] * gg[e];
+          s1 += dxh[k][e];
+          s2 += dxh[k][e] * xh[k][e];
+          ag[k][e] += d[e] * xh[k][e];
+          ab[k][e] += d[e];
+        }
+      }
+    }
+    const float2 sm = group_sum2(s1, s2, red[par][grp], lt, RG, 1 + grp);
+    par ^= 1;
+    const float m1 = sm.x / h, m2 = sm.y / h;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = lt + k * RG;
+      if (vi < nvec) {
+        float o[V];
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
+        if constexpr (DRES) {
+          float q[V];
+          ld_vec(dres + row * h + vi * V, q);
+#pragma unroll
+          for (int e = 0; e < V; ++e) {
+            o[e] += q[e];
+            if constexpr (SUMS) ar[k][e] += q[e];
+          }
+        }
+        st_vec(dx + row * h + vi * V, o);
+        if constexpr (SUMS) {
+          round_as<T>(o);   // the bias gradient sums the stored values
+#pragma unroll
+          for (int e = 0; e < V; ++e) ax[k][e] += o[e];
+        }
+      }
+    }
+  }
+  float* dst = part + (size_t)blockIdx.x * NACC * h;
+  if (NG == 1) {   // one group: its partials are the CTA's
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const int vi = lt + k * RG;
+      if (vi < nvec) {
+#pragma unroll
+        for (int e = 0; e < V; e += 4) {
+          st_vec(dst + vi * V + e, &ag[k][e]);
+          st_vec(dst + h + vi * V + e, &ab[k][e]);
+          if constexpr (SUMS) { st_vec(dst + 2 * h + vi * V + e, &ar[k][e]); st_vec(dst + 3 * h + vi * V + e, &ax[k][e]); }
+        }
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int vi = lt + k * RG;
+    if (vi < nvec)
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        xh[k][e] = (xv[e] - mu) * rs;
-        dxh[k][e] = d[e] * gg[e];
-        s1 += dxh[k][e];
-        s2 += dxh[k][e] * xh[k][e];
+        atomicAdd(&sacc[vi * V + e], ag[k][e]);
+        atomicAdd(&sacc[h + vi * V + e], ab[k][e]);
+        if constexpr (SUMS) {
+          atomicAdd(&sacc[2 * h + vi * V + e], ar[k][e]);
+          atomicAdd(&sacc[3 * h + vi * V + e], ax[k][e]);
+        }
       }
-    }
   }
-  const float2 sm = block_sum2(s1, s2, red);
-  const float m1 = sm.x / h, m2 = sm.y / h;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      float o[V];
-#pragma unroll
-      for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
-      if (dres) {
-        float q[V];
-        ld_vec(dres + row * h + vi * V, q);
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] += q[e];
-      }
-      st_vec(dx + row * h + vi * V, o);
-    }
+  __syncthreads();
+  for (int j = threadIdx.x * 4; j < NACC * h; j += blockDim.x * 4)
+    *reinterpret_cast<float4*>(dst + j) = *reinterpret_cast<const float4*>(sacc + j);
+}
+
+// out_a[n] += sum_c part[c][a][n] for the non-null outputs out_0..out_{nacc-1}.
+// CTA: 32 columns x 8 slices of the G partial rows, slices combined in shared memory.
+__global__ void __launch_bounds__(256) ln_part_reduce_kernel(const float* __restrict__ part, int G, int h, int nacc,
+                                                            float* o0, float* o1, float* o2, float* o3) {
+  __shared__ float red[8][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const int j = blockIdx.x * 32 + tx;
+  const long long ld = (long long)nacc * h;
+  float s0 = 0.f, s1 = 0.f;
+  if (j < nacc * h) {
+    int c = ty;
+    for (; c + 8 < G; c += 16) { s0 += part[c * ld + j]; s1 += part[(c + 8) * ld + j]; }
+    if (c < G) s0 += part[c * ld + j];
   }
+  red[ty][tx] = s0 + s1;
+  __syncthreads();
+  if (ty == 0 && j < nacc * h) {
+    float s = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) s += red[y][tx];
+    const int a = j / h, n = j - a * h;
+    float* o = a == 0 ? o0 : a == 1 ? o1 : a == 2 ? o2 : o3;
+    if (o) o[n] += s;
   }
 }
+
+// CTAs of the backward grid (and rows of partials): at most 2 per SM.
+static int ln_bwd_max_ctas() { return 2 * num_sms(); }
 
 // Column-reduction tiling shared by the bias / gamma / beta gradient kernels:
 // a CTA is CT_X column vectors x CT_Y row groups and covers CT_ROWS rows; a
@@ -416,53 +577,65 @@ mp_status dropout_colsum(const T* dY, T* dZ, float* out, int R, int N, Dropout d
   LAUNCH_CHECK();
 }
 
-// dgamma[n] += sum_r dy[r,n] (x[r,n] - mean[r]) rstd[r];  dbeta[n] += sum_r dy[r,n]
-template <class T>
-__global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                               const float* __restrict__ mean,
-                                                               const float* __restrict__ rstd,
-                                                               float* __restrict__ dgamma, float* __restrict__ dbeta,
-                                                               int R, int h) {
-  constexpr int V = VW<T>::N;
-  __shared__ float red[CT_Y * CT_X * V];
-  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
-  const int nv = h / V, vi = blockIdx.x * CT_X + tx;
-  const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
-  float ag[V] = {}, ab[V] = {};
-  if (vi < nv) {
-#pragma unroll 4
-    for (int r = r0 + ty; r < r1; r += CT_Y) {
-      float d[V], xv[V];
-      ld_vec(dy + (long long)r * h + vi * V, d);
-      ld_vec(x + (long long)r * h + vi * V, xv);
-      const float mu = mean[r], rs = rstd[r];
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        ag[e] += d[e] * (xv[e] - mu) * rs;
-        ab[e] += d[e];
-      }
-    }
+template <class T, int NV, bool RED, bool DRES, bool SUMS>
+static void launch_ln_bwd(const RowCfg& rc, const T* dy, const T* x, const T* g, const float* mean,
+                          const float* rstd, const T* dres, T* dx, T* dy_copy, float* part, int h, int R,
+                          cudaStream_t st, int* grid_out) {
+  auto kern = ln_bwd_kernel<T, NV, RED, DRES, SUMS>;
+  const int threads = rc.RG * rc.NG;
+  const size_t smem = rc.NG > 1 ? sizeof(float) * (SUMS ? 4 : 2) * h : 0;
+  static int attr_set = -1;   // dynamic shared memory above 48 KB needs the opt-in (h up to 16384)
+  if (smem > 48 * 1024 && attr_set < (int)smem) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = (int)smem;
   }
-  ct_reduce_add<V>(ag, red, dgamma, vi, nv);
-  __syncthreads();
-  ct_reduce_add<V>(ab, red, dbeta, vi, nv);
+  const long long need = (R + rc.NG - 1) / rc.NG;
+  const int occ = std::min(2, resident_ctas(kern, threads, smem));
+  const int grid = (int)std::min<long long>(need, std::min<long long>(ln_bwd_max_ctas(), (long long)num_sms() * occ));
+  kern<<<grid, threads, smem, st>>>(dy, x, g, mean, rstd, dres, dx, dy_copy, part, h, R, rc.RG, rc.NG);
+  *grid_out = grid;
+}
+
+template <class T, bool RED, bool DRES, bool SUMS>
+static void ln_bwd_nv(const RowCfg& rc, const T* dy, const T* x, const T* g, const float* mean, const float* rstd,
+                      const T* dres, T* dx, T* dy_copy, float* part, int h, int R, cudaStream_t st, int* grid) {
+#define LNB_NV(NV) launch_ln_bwd<T, NV, RED, DRES, SUMS>(rc, dy, x, g, mean, rstd, dres, dx, dy_copy, part, h, R, st, grid)
+  switch (rc.NV) {
+    case 1: LNB_NV(1); break;
+    case 2: LNB_NV(2); break;
+    case 3: LNB_NV(3); break;
+    case 4: LNB_NV(4); break;
+    default: LNB_NV(8); break;
+  }
+#undef LNB_NV
+}
+
+long long layernorm_bwd_scratch_floats(int R, int h) {
+  (void)R;
+  return (long long)ln_bwd_max_ctas() * 4 * h;
 }
 
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
-                        T* dx, float* dgamma, float* dbeta, float* /*scratch (unused)*/, int R, int h,
-                        cudaStream_t st, T* dy_copy) {
+                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st,
+                        T* dy_copy, float* dres_sum, float* dx_sum) {
   MP_TRY(check_row_dims<T>(R, h));
+  if (!scratch) return set_err(MP_EINVAL, "layernorm_bwd: scratch of layernorm_bwd_scratch_floats() floats required");
+  if ((dres_sum || dx_sum) && !dres) return set_err(MP_EINVAL, "layernorm_bwd: column sums need dres");
+  const RowCfg rc = row_cfg<T>(h);
+  const bool sums = dres_sum || dx_sum;
+  int grid = 0;
+  // dispatch on (RED, DRES, SUMS); SUMS implies DRES
+#define LNB(RED, DRES, SUMS) ln_bwd_nv<T, RED, DRES, SUMS>(rc, dy, x, g, mean, rstd, dres, dx, dy_copy, scratch, h, R, st, &grid)
   if (dy_copy) {
-    ln_bwd_dx_kernel<T, true><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd,
-                                                                                               dres, dx, h, dy_copy, R);
-    dy = dy_copy;
+    if (sums) LNB(true, true, true); else if (dres) LNB(true, true, false); else LNB(true, false, false);
   } else {
-    ln_bwd_dx_kernel<T><<<row_grid(R, h / VW<T>::N), row_threads(h / VW<T>::N), 0, st>>>(dy, x, g, mean, rstd, dres, dx,
-                                                                                         h, nullptr, R);
+    if (sums) LNB(false, true, true); else if (dres) LNB(false, true, false); else LNB(false, false, false);
   }
+#undef LNB
   count_launch();
-  ln_bwd_gb_kernel<T><<<ct_grid(h / VW<T>::N, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dgamma, dbeta, R, h);
+  const int nacc = sums ? 4 : 2;
+  ln_part_reduce_kernel<<<(nacc * h + 31) / 32, 256, 0, st>>>(scratch, grid, h, nacc, dgamma, dbeta, dres_sum, dx_sum);
   LAUNCH_CHECK();
 }
 
@@ -859,6 +1032,84 @@ mp_status ce_loss_grad(const float* logits, const float* rowmax, const float* su
   LAUNCH_CHECK();
 }
 
+// Cross-entropy on the bf16 path (a18): the logit GEMM's epilogue has
+// written bf16 logits, per-(row, column block) partials (max, sum exp(x - max))
+// of the unrounded fp32 logits and the fp32 target logit of owned labels.
+// ce_stats: one warp per row combines the np partials into this shard's row
+// max (mx, and mx_local when a TP max-reduction follows) and sum-exp relative
+// to it (stt[r]); stt[R + r] = the target logit if the label is in the shard.
+__global__ void ce_stats_kernel(const float2* __restrict__ part, int np, const float* __restrict__ tgt,
+                                const int* __restrict__ lab, int lab_ld, int b, int v0, int Vr,
+                                float* __restrict__ mx, float* __restrict__ mx_local, float* __restrict__ stt,
+                                int R) {
+  const int lane = threadIdx.x % 32;
+  const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  if (row >= R) return;
+  const float2* p = part + (long long)row * np;
+  float m = -FLT_MAX;
+  for (int j = lane; j < np; j += 32) m = fmaxf(m, p[j].x);
+  m = warp_max(m);
+  float s = 0.f;
+  for (int j = lane; j < np; j += 32) {
+    const float2 q = p[j];
+    if (q.y > 0.f) s += q.y * exp2f((q.x - m) * 1.4426950408889634f);
+  }
+  s = warp_sum(s);
+  if (lane == 0) {
+    mx[row] = m;
+    if (mx_local) mx_local[row] = m;
+    stt[row] = s;
+    const int id = ce_label(lab, lab_ld, row, b) - v0;
+    stt[R + row] = (id >= 0 && id < Vr) ? tgt[row] : 0.f;
+  }
+}
+
+// after the TP max-reduction of mx: sum-exp relative to the global row max
+__global__ void ce_rescale_kernel(const float* __restrict__ mx, const float* __restrict__ mx_local,
+                                  float* __restrict__ stt, int R) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < R) stt[r] *= exp2f((mx_local[r] - mx[r]) * 1.4426950408889634f);
+}
+
+mp_status ce_stats(const float2* part, int np, const float* tgt, const int* lab, int lab_ld, int b, int v0, int Vr,
+                   float* mx, float* mx_local, float* stt, int R, cudaStream_t st) {
+  ce_stats_kernel<<<(R + 7) / 8, 256, 0, st>>>(part, np, tgt, lab, lab_ld, b, v0, Vr, mx, mx_local, stt, R);
+  LAUNCH_CHECK();
+}
+mp_status ce_rescale(const float* mx, const float* mx_local, float* stt, int R, cudaStream_t st) {
+  ce_rescale_kernel<<<(R + 255) / 256, 256, 0, st>>>(mx, mx_local, stt, R);
+  LAUNCH_CHECK();
+}
+
+// dlogits = (softmax - onehot) * scale, in place over the bf16 logits (one read
+// and one write of the shard, 16-byte vectors); loss += scale (log S + max - target).
+__global__ void __launch_bounds__(256) ce_grad_inplace_kernel(__nv_bfloat16* __restrict__ L,
+                                                              const float* __restrict__ rowmax,
+                                                              const float* __restrict__ st, const int* __restrict__ lab,
+                                                              int lab_ld, int b, int v0, float scale,
+                                                              float* __restrict__ loss_acc, int R, int Vr) {
+  const int row = blockIdx.x;
+  __nv_bfloat16* p = L + (long long)row * Vr;
+  const float mxl2 = rowmax[row] * 1.4426950408889634f, sum = st[row];
+  const float inv = scale / sum;
+  const int id = ce_label(lab, lab_ld, row, b) - v0;
+  if (threadIdx.x == 0) atomicAdd(loss_acc, scale * (logf(sum) + rowmax[row] - st[R + row]));
+  for (int j = threadIdx.x * 8; j < Vr; j += blockDim.x * 8) {
+    float v[8];
+    ld_vec(p + j, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = exp2f(fmaf(v[e], 1.4426950408889634f, -mxl2)) * inv - (j + e == id ? scale : 0.f);
+    st_vec(p + j, v);
+  }
+}
+
+mp_status ce_grad_inplace(__nv_bfloat16* logits, const float* rowmax, const float* sum_tgt, const int* lab, int lab_ld,
+                          int b, int v0, float scale, float* loss_acc, int R, int Vr, cudaStream_t st) {
+  if (Vr % 8) return set_err(MP_EINVAL, "ce: Vr %% 8");
+  ce_grad_inplace_kernel<<<R, 256, 0, st>>>(logits, rowmax, sum_tgt, lab, lab_ld, b, v0, scale, loss_acc, R, Vr);
+  LAUNCH_CHECK();
+}
+
 // ------------------------------------------------------------------ Adam
 template <class T>
 __device__ __forceinline__ void adam_elem(float& w, float g, float& m1, float& m2, T& ws, float lr, float b1, float b2,
@@ -937,7 +1188,7 @@ mp_status cast_from_f32(const float* src, T* dst, long long n, cudaStream_t st) 
   template mp_status dropout_colsum<T>(const T*, T*, float*, int, int, Dropout, cudaStream_t);                      \
   template mp_status attn_dropout<T>(const T*, T*, long long, int, Dropout, cudaStream_t);                          \
   template mp_status layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*,        \
-                                      float*, float*, float*, int, int, cudaStream_t, T*);                          \
+                                      float*, float*, float*, int, int, cudaStream_t, T*, float*, float*);          \
   template mp_status bias_gelu_fwd<T>(const T*, const T*, T*, long long, int, cudaStream_t);                         \
   template mp_status bias_gelu_bwd<T>(const T*, const T*, const T*, T*, float*, int, int, cudaStream_t);             \
   template mp_status colsum_accum<T>(const T*, float*, int, int, cudaStream_t);                                     \

@@ -22,11 +22,11 @@
 #include "common.h"
 #include "kernels.cuh"
 #include "layer.h"
+#include "gemm.h"
 #include "../../include/mp_ops.h"
 
 namespace mp {
 
-mp_status gemm(mp_dtype dt, const mp_gemm_desc& g, cudaStream_t st);
 mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int heads, int hd, cudaStream_t st,
                          Dropout dp);
 long long flash_bwd_ws_floats(int s, int b, int heads, int hd);
@@ -98,7 +98,6 @@ static mp_status lin_dgrad_dgelu(mp_ctx* c, const void* dY, const void* W, const
   g.act = 2; g.C2 = const_cast<void*>(U); g.colsum = db;
   return gemm(c->cfg.dtype, g, c->cs);
 }
-void gemm_set_max_ctas(int n);
 // dW[N, K] += dY[T, N]^T X[T, K]  (fp32 accumulators)
 static mp_status lin_wgrad(mp_ctx* c, const void* dY, const void* X, float* dW, int T, int N, int K,
                            cudaStream_t st = nullptr) {
@@ -164,7 +163,7 @@ mp_status ensure_workspace(mp_ctx* c, int b) {
                     (size_t)d.T * d.h * es, (size_t)d.T * d.h * es, (size_t)d.T * d.h3t * es,
                     (size_t)d.T * d.ht * es};
   for (int i = 0; i < 7; ++i) MP_CUDA(cudaMalloc(bufs[i], al256(sizes[i])));
-  MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * std::max(1LL, mp_op_layernorm_bwd_scratch_floats(d.T, d.h)))));
+  MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * std::max(1LL, layernorm_bwd_scratch_floats(d.T, d.h)))));
   if (fused) MP_CUDA(cudaMalloc(&c->ws_fa, al256(sizeof(float) * (size_t)flash_bwd_ws_floats(d.s, d.b, d.heads, d.hd))));
   c->ws_b = b;
   return MP_OK;
@@ -337,12 +336,11 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   const Dropout dpa = make_dropout(c, layer, 0, st.seq0, st.b), dp1 = make_dropout(c, layer, 1, st.seq0, st.b),
                 dp2 = make_dropout(c, layer, 2, st.seq0, st.b);
   // MLP: dZ2 = dropout mask * dY; db2; dH = dZ2 W2; dW2 += H^T dZ2
+  // without dropout db2 = colsum(dY) is taken by the LN2 backward, which reads dY as its residual input
   const T* dZ2 = dY;
   if (dp2.on()) {
     MP_TRY(dropout_colsum<T>(dY, (T*)c->ws_z, gptr(c, lp[P_B2]), d.T, d.h, dp2, c->cs));
     dZ2 = (const T*)c->ws_z;
-  } else {
-    MP_TRY(colsum_accum<T>(dY, gptr(c, lp[P_B2]), d.T, d.h, c->cs));
   }
   if (fuse_gelu(c)) {      // Y1 holds the biased pre-activation; GeLU backward + db1 in the dgrad epilogue
     MP_TRY(lin_dgrad_dgelu(c, dZ2, ptr<T>(c, lp[P_W2]), st.Y1, dU, gptr(c, lp[P_B1]), d.T, d.h, d.h4t));
@@ -379,16 +377,16 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   } else {
     MP_TRY(lin_wgrad(c, dU, st.A2, gptr(c, lp[P_W1]), d.T, d.h4t, d.h));
   }
+  // dX1 = LN2'(dA2) + dY, with db2 = colsum(dY) and dbo = colsum(dX1) (no dropout) in the same pass
   MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
                           gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs,
-                          nvr ? dA2 : nullptr));
+                          nvr ? dA2 : nullptr, dp2.on() ? nullptr : gptr(c, lp[P_B2]),
+                          dp1.on() ? nullptr : gptr(c, lp[P_BO])));
   // attention block: dZ1 = dropout mask * dX1; dbo; dctx = dZ1 Wo; dWo += ctx^T dZ1
   const T* dZ1 = dX1;
   if (dp1.on()) {
     MP_TRY(dropout_colsum<T>(dX1, (T*)c->ws_z, gptr(c, lp[P_BO]), d.T, d.h, dp1, c->cs));
     dZ1 = (const T*)c->ws_z;
-  } else {
-    MP_TRY(colsum_accum<T>(dX1, gptr(c, lp[P_BO]), d.T, d.h, c->cs));
   }
   if (nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));   // dW1 done before dU / A2 are reused
   MP_TRY(lin_dgrad(c, dZ1, ptr<T>(c, lp[P_WO]), c->ws_dctx, d.T, d.h, d.ht));
@@ -476,6 +474,65 @@ mp_status embed_backward(mp_ctx* c, const int* dtok, int tok_ld, int b, const vo
 // vocab-parallel cross-entropy (TP all-reduces of row max, sum-exp and
 // target logit); dlogits = (softmax - onehot) * scale; dZ = dlogits E_r
 // (f: all-reduce); dE_r += dlogits^T Z; dX = LN_f'(dZ).  loss += scale * sum.
+// bf16 head: the logit GEMM writes bf16 logits and, in its epilogue, the
+// cross-entropy row statistics of the fp32 accumulators (max and sum-exp
+// partials per column block, target logit); one combine kernel and one
+// in-place gradient pass follow (HBM: logits written once, read once, dlogits
+// written once -- instead of fp32 logits read by three passes).
+static mp_status head_bf16(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
+  using T = __nv_bfloat16;
+  const int s = c->cfg.s, h = c->cfg.h, Tn = s * b, Vr = c->cfg.V / c->t;
+  const int ie = c->param_index.at("emb#-1"), ig = c->param_index.at("lnf_g#-1"), ib = c->param_index.at("lnf_b#-1");
+  mp_gemm_desc lg{};
+  lg.M = Tn; lg.N = Vr; lg.K = h; lg.batch = 1;
+  lg.B = ptr<T>(c, ie); lg.lda = h; lg.ldb = h; lg.ldc = Vr; lg.alpha = 1.f;
+  const int np = 2 * gemm_ce_nblocks(lg);
+  size_t o_Z = 0, o_mu = o_Z + al256(2ull * Tn * h), o_rs = o_mu + al256(4ull * Tn), o_L = o_rs + al256(4ull * Tn),
+         o_P = o_L + al256(2ull * Tn * Vr), o_tg = o_P + al256(8ull * Tn * np), o_mx = o_tg + al256(4ull * Tn),
+         o_ml = o_mx + al256(4ull * Tn), o_st = o_ml + al256(4ull * Tn), o_dZ = o_st + al256(8ull * Tn),
+         tot = o_dZ + al256(2ull * Tn * h);
+  void* blk = nullptr;
+  MP_TRY(alloc_async(c, &blk, tot, c->cs));
+  char* base = (char*)blk;
+  T* Z = (T*)(base + o_Z);
+  float *mu = (float*)(base + o_mu), *rs = (float*)(base + o_rs);
+  T* L = (T*)(base + o_L);
+  float2* part = (float2*)(base + o_P);
+  float *tgt = (float*)(base + o_tg), *mx = (float*)(base + o_mx), *mxl = (float*)(base + o_ml),
+        *stt = (float*)(base + o_st);
+  T* dZ = (T*)(base + o_dZ);
+  MP_TRY(layernorm_fwd<T>((const T*)X, ptr<T>(c, ig), ptr<T>(c, ib), Z, mu, rs, Tn, h, c->cfg.ln_eps, c->cs));
+  lg.A = Z; lg.C = L;
+  const GemmCe ce{part, tgt, dlab, lab_ld, b, c->tp * Vr};
+  MP_TRY(gemm(c->cfg.dtype, lg, c->cs, &ce));   // logits = Z E_r^T (+ CE statistics)
+  MP_TRY(ce_stats(part, np, tgt, dlab, lab_ld, b, c->tp * Vr, Vr, mx, c->t > 1 ? mxl : nullptr, stt, Tn, c->cs));
+  if (c->t > 1) {
+    MP_TRY(nccl_check(ncclAllReduce(mx, mx, Tn, ncclFloat32, ncclMax, c->tp_comm, c->cs), "ce max"));
+    MP_TRY(ce_rescale(mx, mxl, stt, Tn, c->cs));
+    MP_TRY(nccl_check(ncclAllReduce(stt, stt, 2 * Tn, ncclFloat32, ncclSum, c->tp_comm, c->cs), "ce sum"));
+  }
+  MP_TRY(ce_grad_inplace(L, mx, stt, dlab, lab_ld, b, c->tp * Vr, scale, c->d_loss, Tn, Vr, c->cs));
+  T* dL = L;
+  {  // dZ = dlogits E_r
+    mp_gemm_desc g{};
+    g.M = Tn; g.N = h; g.K = Vr; g.batch = 1;
+    g.A = dL; g.lda = Vr; g.B = ptr<T>(c, ie); g.ldb = h; g.b_major = 1; g.C = dZ; g.ldc = h; g.alpha = 1.f;
+    MP_TRY(gemm(c->cfg.dtype, g, c->cs));
+  }
+  MP_TRY(allreduce(c, dZ, (size_t)Tn * h, c->cs));                              // f
+  {  // dE_r += dlogits^T Z
+    mp_gemm_desc g{};
+    g.M = Vr; g.N = h; g.K = Tn; g.batch = 1;
+    g.A = dL; g.lda = Vr; g.a_major = 1; g.B = Z; g.ldb = h; g.b_major = 1;
+    g.C = gptr(c, ie); g.ldc = h; g.c_fp32 = 1; g.accumulate = 1; g.alpha = 1.f;
+    MP_TRY(gemm(c->cfg.dtype, g, c->cs));
+  }
+  MP_TRY(layernorm_bwd<T>(dZ, (const T*)X, ptr<T>(c, ig), mu, rs, nullptr, (T*)dX,
+                          gptr(c, ig), gptr(c, ib), c->ws_ln, Tn, h, c->cs));
+  MP_CUDA(cudaFreeAsync(blk, c->cs));
+  return MP_OK;
+}
+
 template <class T>
 static mp_status head_t(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
   const int s = c->cfg.s, h = c->cfg.h, Tn = s * b, Vr = c->cfg.V / c->t;
@@ -527,6 +584,8 @@ static mp_status head_t(mp_ctx* c, const void* X, const int* dlab, int lab_ld, i
 
 mp_status head_fwd_bwd(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
   MP_TRY(ensure_workspace(c, b));
+  static const bool legacy = getenv("MP_HEAD_FP32_LOGITS") != nullptr;   // A/B: round-1 three-pass head
+  if (c->cfg.dtype == MP_BF16 && !legacy) return head_bf16(c, X, dlab, lab_ld, b, scale, dX);
   return c->cfg.dtype == MP_BF16 ? head_t<__nv_bfloat16>(c, X, dlab, lab_ld, b, scale, dX)
                                  : head_t<float>(c, X, dlab, lab_ld, b, scale, dX);
 }

@@ -18,8 +18,10 @@ def f32(n):
 
 
 @pytest.mark.parametrize("dtype", DT)
-@pytest.mark.parametrize("R,h", [(32, 64), (300, 2304), (64, 8192 // 2)])
+@pytest.mark.parametrize("R,h", [(32, 64), (300, 2304), (64, 8192 // 2), (4096, 2304), (333, 6144), (40, 8192), (7, 16384)])
 def test_layernorm_fwd_bwd(dtype, R, h):
+    if dtype == "fp32" and h > 8192:
+        pytest.skip("fp32 rows are limited to h <= 8192")
     x = gen.activations((R, h), 1, 1.0, dtype)
     g = gen.round_to(1 + 0.1 * np.random.default_rng(0).standard_normal(h), dtype)
     b = gen.activations((h,), 2, 0.1, dtype)
@@ -43,6 +45,22 @@ def test_layernorm_fwd_bwd(dtype, R, h):
     assert normwise(host(dx_), dxr + dres) < TOL[dtype] / 4
     assert normwise(host(dg), dgr) < TOL[dtype] / 4
     assert normwise(host(db), dbr) < TOL[dtype] / 4
+    # the one-pass variant that also takes the two bias gradients around LN2 (b2 = colsum of the
+    # residual input dres, bo = colsum of the stored dx); accumulators start non-zero (+=)
+    acc0 = gen.activations((4, h), 11, 1.0, "fp32")
+    acc = dev(acc0, "fp32")
+    dx2 = dev(np.zeros((R, h)), dtype)
+    mp.call("mp_op_layernorm_bwd_sums", dtype, dyd.data_ptr(), xd.data_ptr(), gd.data_ptr(), mu.data_ptr(),
+            rs.data_ptr(), dresd.data_ptr(), dx2.data_ptr(), acc[0].data_ptr(), acc[1].data_ptr(),
+            acc[2].data_ptr(), acc[3].data_ptr(), scratch.data_ptr(), R, h, None)
+    torch.cuda.synchronize()
+    got = host(acc)
+    assert np.array_equal(host(dx2), host(dx_))            # same dx, bit for bit
+    assert normwise(got[0] - acc0[0], dgr) < TOL[dtype] / 4
+    assert normwise(got[1] - acc0[1], dbr) < TOL[dtype] / 4
+    assert normwise(got[2] - acc0[2], dres.sum(0)) < TOL[dtype] / 4
+    assert normwise(got[3] - acc0[3], host(dx2).sum(0)) < TOL[dtype] / 4
+    assert normwise(got[3] - acc0[3], (dxr + dres).sum(0)) < TOL[dtype]
 
 
 @pytest.mark.parametrize("dtype", DT)
