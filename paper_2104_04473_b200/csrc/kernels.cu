@@ -279,8 +279,13 @@ static mp_status launch_ln_fwd(const T* in, const T* bias, const T* res, T* x1, 
 }
 
 template <class T>
+static mp_status ln_fwd_v1(int mode, bool red, const T* in, const T* bias, const T* res, T* x1, const T* g, const T* b,
+                           T* out, float* mean, float* rstd, int R, int h, float eps, Dropout dp, cudaStream_t st);
+static bool ln_v1();
+template <class T>
 mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int R, int h, float eps,
                         cudaStream_t st) {
+  if (ln_v1()) return ln_fwd_v1<T>(0, false, x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, R, h, eps, Dropout{}, st);
   return launch_ln_fwd<T, 0, false>(x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, R, h, eps, Dropout{}, st);
 }
 
@@ -288,6 +293,7 @@ template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
                             float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp,
                             bool red) {
+  if (ln_v1()) return ln_fwd_v1<T>(1, red, yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
   if (red) return launch_ln_fwd<T, 1, true>(yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
   return launch_ln_fwd<T, 1, false>(yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
 }
@@ -577,6 +583,210 @@ mp_status dropout_colsum(const T* dY, T* dZ, float* out, int R, int N, Dropout d
   LAUNCH_CHECK();
 }
 
+// ---------------------------------------------------- round-1 row kernels
+// (A/B reference only: MP_LN_V1=1 selects them; one CTA per row, block-wide sums)
+static int row_threads_v1(int nvec) {
+  int t = ((nvec + 3) / 4 + 31) / 32 * 32;   // <= 4 vectors per thread
+  return std::max(32, std::min(256, t));
+}
+constexpr int LN_MAXV_V1 = 4;
+// Grid of a row kernel: every row handled by one CTA in a grid-stride loop, the grid
+// sized to the CTAs that are resident at once (<= 64 warps / 32 CTAs per SM), so there
+// is no partial last wave (T = 4096 rows of 96 threads would be 1.3 waves).
+static int row_grid_v1(long long R, int nvec) {
+  const int warps = row_threads_v1(nvec) / 32;
+  const int per_sm = std::max(1, std::min(32, 64 / warps));
+  return (int)std::max(1LL, std::min<long long>(R, (long long)num_sms() * per_sm));
+}
+
+// mode 0: x = in; mode 1: x = r + yv + bias (bias-dropout-add with p = 0), x1 <- x.
+template <class T, int MODE, bool RED = false>
+__global__ void __launch_bounds__(256) ln_fwd_kernel_v1(const T* __restrict__ in, const T* __restrict__ bias,
+                                                     const T* __restrict__ res, T* __restrict__ x1,
+                                                     const T* __restrict__ g, const T* __restrict__ b,
+                                                     T* __restrict__ out, float* __restrict__ mean,
+                                                     float* __restrict__ rstd, int h, float eps, Dropout dp, int R) {
+  constexpr int V = VW<T>::N;
+  __shared__ float2 red[32];
+  const int nvec = h / V;
+  // grid-stride over rows: a grid of a few resident CTAs per SM, no partial last wave
+  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
+  float v[LN_MAXV_V1][V];
+  float s1 = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV_V1; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      ld_in<RED>(in + row * h + vi * V, v[k]);
+      if (MODE == 1) {
+        float bb[V], rr[V];
+        ld_vec(bias + vi * V, bb);
+        ld_vec(res + row * h + vi * V, rr);
+        if (dp.on()) {   // x1 = r + dropout(y + bias), mask keyed by (sequence, position, feature)
+          const int pos = (int)(row / dp.b), seq = dp.seq0 + (int)(row % dp.b);
+          const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * h + vi * V, 0, seq);
+#pragma unroll
+          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + ((km >> e) & 1 ? (v[k][e] + bb[e]) * dp.scale : 0.f);
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
+        }
+        st_vec(x1 + row * h + vi * V, v[k]);
+        // LayerNorm consumes the stored (rounded) residual stream value
+        ld_vec(x1 + row * h + vi * V, v[k]);
+      }
+#pragma unroll
+      for (int e = 0; e < V; ++e) s1 += v[k][e];
+    }
+  }
+  const float mu = block_sum2(s1, 0.f, red).x / h;
+  float s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV_V1; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec)
+#pragma unroll
+      for (int e = 0; e < V; ++e) { float d = v[k][e] - mu; s2 += d * d; }
+  }
+  const float var = block_sum2(s2, 0.f, red).x / h;
+  const float rs = rsqrtf(var + eps);
+#pragma unroll
+  for (int k = 0; k < LN_MAXV_V1; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float gg[V], bb[V], o[V];
+      ld_vec(g + vi * V, gg);
+      ld_vec(b + vi * V, bb);
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = (v[k][e] - mu) * rs * gg[e] + bb[e];
+      st_vec(out + row * h + vi * V, o);
+    }
+  }
+  if (threadIdx.x == 0) { mean[row] = mu; rstd[row] = rs; }
+  }
+}
+
+// dx: one CTA per row (fp32 block sums of dxhat and dxhat*xhat).
+// RED: dy is a multicast address (NVLS reduce-load of the TP partial sums); the
+// reduced rows are also stored to dy_copy for the gamma/beta kernel.
+template <class T, bool RED = false>
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel_v1(const T* __restrict__ dy, const T* __restrict__ x,
+                                                        const T* __restrict__ g, const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy, int R) {
+  constexpr int V = VW<T>::N;
+  __shared__ float2 red[32];
+  const int nvec = h / V;
+  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
+  const float mu = mean[row], rs = rstd[row];
+  float xh[LN_MAXV_V1][V], dxh[LN_MAXV_V1][V];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV_V1; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float d[V], xv[V], gg[V];
+      ld_in<RED>(dy + row * h + vi * V, d);
+      if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
+      ld_vec(x + row * h + vi * V, xv);
+      ld_vec(g + vi * V, gg);
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        xh[k][e] = (xv[e] - mu) * rs;
+        dxh[k][e] = d[e] * gg[e];
+        s1 += dxh[k][e];
+        s2 += dxh[k][e] * xh[k][e];
+      }
+    }
+  }
+  const float2 sm = block_sum2(s1, s2, red);
+  const float m1 = sm.x / h, m2 = sm.y / h;
+#pragma unroll
+  for (int k = 0; k < LN_MAXV_V1; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float o[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
+      if (dres) {
+        float q[V];
+        ld_vec(dres + row * h + vi * V, q);
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] += q[e];
+      }
+      st_vec(dx + row * h + vi * V, o);
+    }
+  }
+  }
+}
+
+// dgamma[n] += sum_r dy[r,n] (x[r,n] - mean[r]) rstd[r];  dbeta[n] += sum_r dy[r,n]
+template <class T>
+__global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel_v1(const T* __restrict__ dy, const T* __restrict__ x,
+                                                               const float* __restrict__ mean,
+                                                               const float* __restrict__ rstd,
+                                                               float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                               int R, int h) {
+  constexpr int V = VW<T>::N;
+  __shared__ float red[CT_Y * CT_X * V];
+  const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
+  const int nv = h / V, vi = blockIdx.x * CT_X + tx;
+  const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
+  float ag[V] = {}, ab[V] = {};
+  if (vi < nv) {
+#pragma unroll 4
+    for (int r = r0 + ty; r < r1; r += CT_Y) {
+      float d[V], xv[V];
+      ld_vec(dy + (long long)r * h + vi * V, d);
+      ld_vec(x + (long long)r * h + vi * V, xv);
+      const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+      for (int e = 0; e < V; ++e) {
+        ag[e] += d[e] * (xv[e] - mu) * rs;
+        ab[e] += d[e];
+      }
+    }
+  }
+  ct_reduce_add<V>(ag, red, dgamma, vi, nv);
+  __syncthreads();
+  ct_reduce_add<V>(ab, red, dbeta, vi, nv);
+}
+
+
+template <class T>
+static mp_status ln_fwd_v1(int mode, bool red, const T* in, const T* bias, const T* res, T* x1, const T* g, const T* b,
+                           T* out, float* mean, float* rstd, int R, int h, float eps, Dropout dp, cudaStream_t st) {
+  const int nv = h / VW<T>::N;
+  if (mode == 0)
+    ln_fwd_kernel_v1<T, 0><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(in, nullptr, nullptr, nullptr, g, b, out, mean, rstd, h, eps, Dropout{}, R);
+  else if (red)
+    ln_fwd_kernel_v1<T, 1, true><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R);
+  else
+    ln_fwd_kernel_v1<T, 1><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R);
+  LAUNCH_CHECK();
+}
+template <class T>
+mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st);
+template <class T>
+static mp_status ln_bwd_v1(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
+                           T* dx, float* dgamma, float* dbeta, int R, int h, cudaStream_t st, T* dy_copy,
+                           float* dres_sum, float* dx_sum) {
+  const int nv = h / VW<T>::N;
+  if (dy_copy) {
+    ln_bwd_dx_kernel_v1<T, true><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, dy_copy, R);
+    dy = dy_copy;
+  } else {
+    ln_bwd_dx_kernel_v1<T><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, nullptr, R);
+  }
+  count_launch();
+  ln_bwd_gb_kernel_v1<T><<<ct_grid(h / VW<T>::N, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dgamma, dbeta, R, h);
+  count_launch();
+  if (dres_sum) MP_TRY(colsum_accum<T>(dres, dres_sum, R, h, st));
+  if (dx_sum) MP_TRY(colsum_accum<T>(dx, dx_sum, R, h, st));
+  return MP_OK;
+}
+static bool ln_v1() { return getenv("MP_LN_V1") != nullptr; }
+
 template <class T, int NV, bool RED, bool DRES, bool SUMS>
 static void launch_ln_bwd(const RowCfg& rc, const T* dy, const T* x, const T* g, const float* mean,
                           const float* rstd, const T* dres, T* dx, T* dy_copy, float* part, int h, int R,
@@ -622,6 +832,7 @@ mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, 
   MP_TRY(check_row_dims<T>(R, h));
   if (!scratch) return set_err(MP_EINVAL, "layernorm_bwd: scratch of layernorm_bwd_scratch_floats() floats required");
   if ((dres_sum || dx_sum) && !dres) return set_err(MP_EINVAL, "layernorm_bwd: column sums need dres");
+  if (ln_v1()) return ln_bwd_v1<T>(dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, R, h, st, dy_copy, dres_sum, dx_sum);
   const RowCfg rc = row_cfg<T>(h);
   const bool sums = dres_sum || dx_sum;
   int grid = 0;

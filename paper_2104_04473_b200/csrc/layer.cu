@@ -479,24 +479,26 @@ mp_status embed_backward(mp_ctx* c, const int* dtok, int tok_ld, int b, const vo
 // partials per column block, target logit); one combine kernel and one
 // in-place gradient pass follow (HBM: logits written once, read once, dlogits
 // written once -- instead of fp32 logits read by three passes).
-static mp_status head_bf16(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
+static mp_status head_bf16(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX,
+                           int defer_slot) {
   using T = __nv_bfloat16;
   const int s = c->cfg.s, h = c->cfg.h, Tn = s * b, Vr = c->cfg.V / c->t;
+  const bool defer = defer_slot >= 0;
   const int ie = c->param_index.at("emb#-1"), ig = c->param_index.at("lnf_g#-1"), ib = c->param_index.at("lnf_b#-1");
   mp_gemm_desc lg{};
   lg.M = Tn; lg.N = Vr; lg.K = h; lg.batch = 1;
   lg.B = ptr<T>(c, ie); lg.lda = h; lg.ldb = h; lg.ldc = Vr; lg.alpha = 1.f;
   const int np = 2 * gemm_ce_nblocks(lg);
-  size_t o_Z = 0, o_mu = o_Z + al256(2ull * Tn * h), o_rs = o_mu + al256(4ull * Tn), o_L = o_rs + al256(4ull * Tn),
-         o_P = o_L + al256(2ull * Tn * Vr), o_tg = o_P + al256(8ull * Tn * np), o_mx = o_tg + al256(4ull * Tn),
+  size_t o_Z = 0, o_mu = o_Z + al256(defer ? 0 : 2ull * Tn * h), o_rs = o_mu + al256(4ull * Tn),
+         o_L = o_rs + al256(4ull * Tn), o_P = o_L + al256(defer ? 0 : 2ull * Tn * Vr), o_tg = o_P + al256(8ull * Tn * np), o_mx = o_tg + al256(4ull * Tn),
          o_ml = o_mx + al256(4ull * Tn), o_st = o_ml + al256(4ull * Tn), o_dZ = o_st + al256(8ull * Tn),
          tot = o_dZ + al256(2ull * Tn * h);
   void* blk = nullptr;
   MP_TRY(alloc_async(c, &blk, tot, c->cs));
   char* base = (char*)blk;
-  T* Z = (T*)(base + o_Z);
+  T* Z = defer ? (T*)c->head_z + (size_t)defer_slot * Tn * h : (T*)(base + o_Z);
   float *mu = (float*)(base + o_mu), *rs = (float*)(base + o_rs);
-  T* L = (T*)(base + o_L);
+  T* L = defer ? (T*)c->head_dl + (size_t)defer_slot * Tn * Vr : (T*)(base + o_L);
   float2* part = (float2*)(base + o_P);
   float *tgt = (float*)(base + o_tg), *mx = (float*)(base + o_mx), *mxl = (float*)(base + o_ml),
         *stt = (float*)(base + o_st);
@@ -520,7 +522,7 @@ static mp_status head_bf16(mp_ctx* c, const void* X, const int* dlab, int lab_ld
     MP_TRY(gemm(c->cfg.dtype, g, c->cs));
   }
   MP_TRY(allreduce(c, dZ, (size_t)Tn * h, c->cs));                              // f
-  {  // dE_r += dlogits^T Z
+  if (!defer) {  // dE_r += dlogits^T Z
     mp_gemm_desc g{};
     g.M = Vr; g.N = h; g.K = Tn; g.batch = 1;
     g.A = dL; g.lda = Vr; g.a_major = 1; g.B = Z; g.ldb = h; g.b_major = 1;
@@ -531,6 +533,22 @@ static mp_status head_bf16(mp_ctx* c, const void* X, const int* dlab, int lab_ld
                           gptr(c, ig), gptr(c, ib), c->ws_ln, Tn, h, c->cs));
   MP_CUDA(cudaFreeAsync(blk, c->cs));
   return MP_OK;
+}
+
+// The logit layer's weight gradient of a whole batch as one GEMM at the flush: the
+// microbatches' dlogits / Z row blocks are contiguous, so sum_mb dL_mb^T Z_mb =
+// [dL_1; ..; dL_m]^T [Z_1; ..; Z_m] (K = m b s): the fp32 dE_r accumulator is read and
+// written once per batch instead of once per microbatch, and the GEMM leaves the
+// last stage's forward tasks (it fills that device's cool-down idle instead).
+mp_status head_dE_deferred(mp_ctx* c, int b, int n_slots) {
+  const int h = c->cfg.h, Vr = c->cfg.V / c->t;
+  const long long K = (long long)n_slots * c->cfg.s * b;
+  if (K > 0x7fffffffLL) return set_err(MP_EINVAL, "deferred dE: K too large");
+  mp_gemm_desc g{};
+  g.M = Vr; g.N = h; g.K = (int)K; g.batch = 1;
+  g.A = c->head_dl; g.lda = Vr; g.a_major = 1; g.B = c->head_z; g.ldb = h; g.b_major = 1;
+  g.C = gptr(c, c->param_index.at("emb#-1")); g.ldc = h; g.c_fp32 = 1; g.accumulate = 1; g.alpha = 1.f;
+  return gemm(c->cfg.dtype, g, c->cs);
 }
 
 template <class T>
@@ -582,10 +600,12 @@ static mp_status head_t(mp_ctx* c, const void* X, const int* dlab, int lab_ld, i
   return MP_OK;
 }
 
-mp_status head_fwd_bwd(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX) {
+mp_status head_fwd_bwd(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX,
+                       int defer_slot) {
   MP_TRY(ensure_workspace(c, b));
   static const bool legacy = getenv("MP_HEAD_FP32_LOGITS") != nullptr;   // A/B: round-1 three-pass head
-  if (c->cfg.dtype == MP_BF16 && !legacy) return head_bf16(c, X, dlab, lab_ld, b, scale, dX);
+  if (c->cfg.dtype == MP_BF16 && !legacy) return head_bf16(c, X, dlab, lab_ld, b, scale, dX, defer_slot);
+  if (defer_slot >= 0) return set_err(MP_EINVAL, "deferred dE needs the bf16 head");
   return c->cfg.dtype == MP_BF16 ? head_t<__nv_bfloat16>(c, X, dlab, lab_ld, b, scale, dX)
                                  : head_t<float>(c, X, dlab, lab_ld, b, scale, dX);
 }

@@ -292,7 +292,7 @@ mp_status mp_finalize(mp_ctx* c) {
   for (auto cm : comms)
     if (cm) ncclCommDestroy(cm);
   void* bufs[] = {c->ws_z, c->ws_dsq, c->ws_d4h, c->ws_dh1, c->ws_dh2, c->ws_dqkv, c->ws_dctx, c->ws_ln, c->ws_fa,
-                  c->grads, c->adam_m, c->adam_v, c->d_loss, c->master};
+                  c->grads, c->adam_m, c->adam_v, c->d_loss, c->master, c->head_dl, c->head_z};
   for (void* q : bufs)
     if (q) cudaFree(q);
   if (c->cfg.dtype == MP_BF16 && c->wstore) cudaFree(c->wstore);
@@ -474,6 +474,27 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   for (const auto& P : c->params)
     if (P.layer < 0) model_off = std::min(model_off, P.off);
 
+  // logit-layer weight gradient deferred to the flush (bf16 last stage): per microbatch
+  // dlogits [T, V/t] and Z [T, h] are kept (MP_HEAD_DEFER_GB bounds the buffers, default 16)
+  bool defer_dE = false;
+  if (c->has_head && c->cfg.dtype == MP_BF16 && !getenv("MP_HEAD_FP32_LOGITS")) {
+    static const double budget = getenv("MP_HEAD_DEFER_GB") ? atof(getenv("MP_HEAD_DEFER_GB")) : 16.0;
+    const size_t dl = (size_t)m * s * b * (size_t)(c->cfg.V / c->t) * 2, zb = (size_t)m * s * b * h * 2;
+    if ((double)(dl + zb) <= budget * 1e9) {
+      defer_dE = true;
+      if (c->head_dl_bytes < dl || c->head_z_bytes < zb) {
+        MP_CUDA(cudaStreamSynchronize(cs));
+        if (c->head_dl) cudaFree(c->head_dl);
+        if (c->head_z) cudaFree(c->head_z);
+        c->head_dl = c->head_z = nullptr;
+        c->head_dl_bytes = c->head_z_bytes = 0;
+        MP_CUDA(cudaMalloc(&c->head_dl, dl));
+        MP_CUDA(cudaMalloc(&c->head_z, zb));
+        c->head_dl_bytes = dl;
+        c->head_z_bytes = zb;
+      }
+    }
+  }
   static const bool dbg = getenv("MP_DEBUG") != nullptr;
   for (const Task& tk : tasks) {
     const int sigma = tk.chunk * p + c->pp;
@@ -517,7 +538,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
       if (sigma == S - 1) {
         void* dx = nullptr;
         MP_TRY(alloc_async(c, &dx, act_bytes, cs));
-        MP_TRY(head_fwd_bwd(c, x, tok + 1, s + 1, b, scale, dx));
+        MP_TRY(head_fwd_bwd(c, x, tok + 1, s + 1, b, scale, dx, defer_dE ? tk.mb : -1));
         MP_CUDA(cudaFreeAsync(x, cs));
         local_grad[{tk.mb, sigma}] = dx;
         MP_CUDA(cudaEventRecord(t1, cs));
@@ -598,6 +619,7 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
   }
   // ------------------------------------------------------------------ flush
   if (dbg) fprintf(stderr, "[mp rank %d] all tasks enqueued\n", c->rank);
+  if (defer_dE) MP_TRY(head_dE_deferred(c, b, m));
   if (p > 1) {
     cudaStream_t ss[] = {c->s_act_send, c->s_grad_send, c->s_act_recv, c->s_grad_recv};
     for (auto q : ss) {

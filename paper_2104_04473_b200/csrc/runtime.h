@@ -87,6 +87,12 @@ struct mp_ctx {
   float* ws_ln = nullptr;
   float* ws_fa = nullptr;          // fused-attention backward workspace (dQ accumulator, D)
   float* d_loss = nullptr;
+  // deferred logit-layer weight gradient (bf16, last stage): every microbatch's dlogits and
+  // final-LN output Z are kept in these row-stacked buffers [m T, V/t] / [m T, h] and
+  // dE_r += dlogits^T Z runs once at the flush as one GEMM with K = m T
+  void* head_dl = nullptr;
+  void* head_z = nullptr;
+  size_t head_dl_bytes = 0, head_z_bytes = 0;
   // events for task timing
   std::vector<cudaEvent_t> events;
   int cur_seq0 = 0;                // set by the batch runtime before each microbatch task

@@ -22,10 +22,23 @@ from paper_2104_04473_b200 import mp  # noqa: E402
 
 
 def timeit(fn, reps, flush=None):
+    """Median kernel time in us.  Warm: `reps` back-to-back launches between two events
+    (host launch overhead overlaps the GPU work).  Cold: a 512 MB write before each
+    launch, only the launch inside the events."""
     st = torch.cuda.current_stream()
     ts = []
     for _ in range(3):
         fn()
+    if flush is None:
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for _ in range(3):
+            a.record(st)
+            for _ in range(reps):
+                fn()
+            b.record(st)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e3 / reps)
+        return min(ts)
     for _ in range(reps):
         if flush is not None:
             flush.fill_(1.0)
@@ -44,6 +57,7 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--R", type=int, default=4096)
     ap.add_argument("--widths", default="2304,4096,6144,8192")
+    ap.add_argument("--ab", action="store_true", help="also time the round-1 kernels (MP_LN_V1=1)")
     args = ap.parse_args()
     mp.lib()
     peak = None
@@ -83,16 +97,20 @@ def main():
         }
         mp.call("mp_op_layernorm_fwd", "bf16", x.data_ptr(), g.data_ptr(), b.data_ptr(), o.data_ptr(),
                 mu.data_ptr(), rs.data_ptr(), R, h, 1e-5, st)
-        for name, (fn, nbytes) in kernels.items():
-            warm = timeit(fn, args.reps)
-            cold = timeit(fn, args.reps, flush)
-            rec = {"kernel": name, "R": R, "h": h, "bytes": nbytes, "warm_us": round(warm, 2),
-                   "cold_us": round(cold, 2), "warm_gbs": round(nbytes / warm / 1e3, 1),
-                   "cold_gbs": round(nbytes / cold / 1e3, 1)}
-            if peak:
-                rec["cold_frac"] = round(nbytes / cold / 1e3 / peak, 3)
-            out.append(rec)
-            print(json.dumps(rec), flush=True)
+        for variant in (["new", "v1"] if args.ab else ["new"]):
+            if variant == "v1":
+                os.environ["MP_LN_V1"] = "1"
+            for name, (fn, nbytes) in kernels.items():
+                warm = timeit(fn, args.reps)
+                cold = timeit(fn, args.reps, flush)
+                rec = {"kernel": name, "variant": variant, "R": R, "h": h, "bytes": nbytes, "warm_us": round(warm, 2),
+                       "cold_us": round(cold, 2), "warm_gbs": round(nbytes / warm / 1e3, 1),
+                       "cold_gbs": round(nbytes / cold / 1e3, 1)}
+                if peak:
+                    rec["cold_frac"] = round(nbytes / cold / 1e3 / peak, 3)
+                out.append(rec)
+                print(json.dumps(rec), flush=True)
+            os.environ.pop("MP_LN_V1", None)
 
 
 if __name__ == "__main__":
