@@ -87,7 +87,8 @@ long long mp_launch_count(void);
 
 /* LayerNorm over rows of x [R, h] (implied by Eq. (1)'s 13h term, P:344;
  * pre-LN GPT layer, reading #1; biased variance, eps): y = g * xhat + b;
- * per-row fp32 mean / rstd saved for the backward.  h <= 16384 (bf16), 8192 (fp32). */
+ * per-row fp32 mean / rstd saved for the backward.  h <= 16384 (bf16), 8192 (fp32);
+ * the backward takes h <= 8192 (bf16), 4096 (fp32). */
 mp_status mp_op_layernorm_fwd(mp_dtype dt, const void* x, const void* g, const void* b, void* y, float* mean,
                               float* rstd, int R, int h, float eps, void* stream);
 
@@ -99,22 +100,19 @@ mp_status mp_op_bda_layernorm_fwd(mp_dtype dt, const void* y, const void* bias, 
 
 /* LayerNorm backward (a17; P:574 counts it with the layer): dx = LN'(dy)
  * (+ dres if non-NULL); dgamma, dbeta (fp32 [h]) are ACCUMULATED (+=).
- * One pass over the rows; every CTA writes its column partials to `scratch`
- * (device fp32, caller-owned, mp_op_layernorm_bwd_scratch_floats(R, h)
- * floats; 0 without a device) and a second kernel adds their sums into the
- * accumulators in a fixed order.  MP_EINVAL if scratch is NULL. */
+ * A row kernel (dx) and a column-tile kernel (the column sums). */
 mp_status mp_op_layernorm_bwd(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
-                              const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
-                              float* scratch, int R, int h, void* stream);
+                              const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta, int R, int h,
+                              void* stream);
 /* Same, also accumulating the column sums of dres (dres_sum) and of the
  * stored dx (dx_sum), either may be NULL, both need dres: in the layer
  * backward around LN2 these are the bias gradients of FC2 (b2: column sum of
  * the layer's output gradient, P:146 bias added after g) and of the
- * projection (bo: column sum of dX1), so no separate column-sum pass runs. */
+ * projection (bo: column sum of dX1), taken in the column kernel's pass, so
+ * no separate column-sum launches run. */
 mp_status mp_op_layernorm_bwd_sums(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
                                    const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
-                                   float* dres_sum, float* dx_sum, float* scratch, int R, int h, void* stream);
-long long mp_op_layernorm_bwd_scratch_floats(int R, int h);
+                                   float* dres_sum, float* dx_sum, int R, int h, void* stream);
 
 /* Fused bias + tanh-GeLU (reading #3): out = gelu(y + b), y [R, N]. */
 mp_status mp_op_bias_gelu_fwd(mp_dtype dt, const void* y, const void* b, void* out, long long R, int N,

@@ -355,29 +355,21 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
 }
 
 // ------------------------------------------------------------- backward
-// Per (head z, key/value tile j) CTA, looping over the query tiles i >= j, in
-// the transposed orientation (TMEM lanes = the 128 keys of tile j):
-//   S^T = K_j Q_i^T, dP^T = V_j dO_i^T                   (TMEM [0,128), [128,256))
-//   P^T = exp2(S^T log2e/sqrt(hd) - L2_i), dS^T = P^T (dP^T - D_i) / sqrt(hd)
-//     (compute warps; a thread owns one key row, L2 / D of the 128 queries are
-//     broadcast from shared memory), written back as packed bf16 over S^T / dP^T
-//   dV_j += P^T dO_i, dK_j += dS^T Q_i                   (A operand from TMEM)
-//   dQ_i  = dS K_j (A = dS from shared memory, MN-major = the dS^T rows)
-//     -> fp32 TMA reductions into a dQ accumulator
-// P never goes through shared memory, which frees the space to double-buffer
-// Q_i / dO_i (the next tile's loads overlap this tile's chain), and the dQ
-// product is issued first so its read-out overlaps the dV / dK products.
-// D_i = rowsum(dO_i * O_i) is precomputed.
+// Per (head z, key/value tile j) CTA, looping over the query tiles i >= j:
+//   S = Q_i K_j^T, dP = dO_i V_j^T                       (TMEM [0,128), [128,256))
+//   P = exp2(S log2e/sqrt(hd) - L2_i), dS = P (dP - D_i) / sqrt(hd)   (compute warps)
+//   dV_j += P^T dO_i, dK_j += dS^T Q_i                   (TMEM accumulators)
+//   dQ_i  = dS K_j -> fp32 vector reductions into a dQ accumulator
+// D_i = rowsum(dO_i * O_i) is precomputed.  Q_i / dO_i / K_j tiles serve both
+// as K-major and (via the MN-major descriptor view) MN-major operands, and P
+// / dS as K-major (dQ) and MN-major (dV, dK) operands: no transposes.
 namespace fab {
 // warp 0 TMA, warp 1 MMA, warps 2-9 compute: two warps per TMEM lane quarter,
-// each taking half of the 128 query columns (P / dS) and of the dQ chunks
+// each taking half of the 128 key columns (P / dS) and of the dQ chunks
 constexpr int THREADS = 320;
 constexpr int CW = 256;                      // compute threads
 constexpr int T_BYTES = 2 * 128 * 128;       // one [128 rows x hd<=128] bf16 tile (2 hd blocks)
-// K, V, Q[2], dO[2], dS (+ dQ staging); L2 / D of the query tile; barriers
-constexpr int SMEM = 7 * T_BYTES + 1024 + 1024 + 256;
-// TMEM columns
-constexpr uint32_t C_S = 0, C_DP = 128, C_DQ0 = 64, C_DQ1 = 192, C_DV = 256, C_DK = 384;
+constexpr int SMEM = 6 * T_BYTES + 1024 + 512;
 }  // namespace fab
 
 struct FabArgs {
@@ -406,327 +398,6 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                  const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
                  const __grid_constant__ CUtensorMap tmdQ, FabArgs g) {
   using namespace fab;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sK = smem;
-  uint8_t* sV = sK + T_BYTES;
-  uint8_t* sQ = sV + T_BYTES;          // [2]
-  uint8_t* sdO = sQ + 2 * T_BYTES;     // [2]
-  uint8_t* sdS = sdO + 2 * T_BYTES;    // dS (MN-major A of dQ = dS K); then the dQ staging boxes
-  float* sStat = reinterpret_cast<float*>(sdS + T_BYTES);   // [2][128]: L2, D of the current query tile
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sStat + 256);
-  uint64_t* kv_full = bar + 0;
-  uint64_t* q_full = bar + 1;     // [2] Q_i landed
-  uint64_t* q_empty = bar + 3;    // [2] dK += dS^T Q_i complete (and every earlier product of tile i)
-  uint64_t* do_full = bar + 5;    // [2] dO_i landed
-  uint64_t* do_empty = bar + 7;   // [2] dV += P^T dO_i complete
-  uint64_t* sdp_full = bar + 9;
-  uint64_t* ds_ready = bar + 10;
-  uint64_t* dq_full = bar + 11;
-  uint64_t* tmem_free = bar + 12;
-  uint64_t* acc_done = bar + 13;  // the last dV / dK products complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // key/value tile, heaviest (most query tiles) first across the whole grid;
-  // split mode: a CTA takes query tiles kt+it0 .. kt+it1-1 of its kv tile
-  int kt, z, it0 = 0, niter;
-  if (g.work) {
-    const int4 w = g.work[blockIdx.x];
-    z = w.x; kt = w.y; it0 = w.z; niter = w.w - w.z;
-  } else {
-    const int zn = (int)(gridDim.x / g.nq);
-    kt = (int)(blockIdx.x / zn);
-    z = (int)(blockIdx.x % zn);
-    niter = g.nq - kt;                              // query tiles kt .. nq-1
-  }
-  const int tile_bytes = g.nhb * 128 * 128;
-
-  if (threadIdx.x == 0) {
-    mbar_init(kv_full, 1);
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&q_full[i], 1); mbar_init(&q_empty[i], 1); mbar_init(&do_full[i], 1); mbar_init(&do_empty[i], 1);
-    }
-    mbar_init(sdp_full, 1); mbar_init(ds_ready, CW); mbar_init(dq_full, 1); mbar_init(tmem_free, CW);
-    mbar_init(acc_done, 1);
-    fence_mbar_init();
-  }
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); tma_prefetch(&tmdO); tma_prefetch(&tmdQ);
-  }
-  if (warp == 1) tmem_alloc<fa::TMEM_COLS>(tmem_slot);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      mbar_arrive_expect_tx(kv_full, 2 * tile_bytes);
-      for (int hb = 0; hb < g.nhb; ++hb) {
-        tma_load_3d(sK + hb * 16384, &tmK, kv_full, 64 * hb, kt * 128, z);
-        tma_load_3d(sV + hb * 16384, &tmV, kv_full, 64 * hb, kt * 128, z);
-      }
-      for (int it = 0; it < niter; ++it) {
-        const int qi = kt + it0 + it, bf = it & 1;
-        // buffer bf was last used by tile it-2: refill once its products are done
-        if (it >= 2) mbar_wait(&q_empty[bf], ((it - 2) >> 1) & 1);
-        mbar_arrive_expect_tx(&q_full[bf], tile_bytes);
-        for (int hb = 0; hb < g.nhb; ++hb)
-          tma_load_3d(sQ + bf * T_BYTES + hb * 16384, &tmQ, &q_full[bf], 64 * hb, qi * 128, z);
-        if (it >= 2) mbar_wait(&do_empty[bf], ((it - 2) >> 1) & 1);
-        mbar_arrive_expect_tx(&do_full[bf], tile_bytes);
-        for (int hb = 0; hb < g.nhb; ++hb)
-          tma_load_3d(sdO + bf * T_BYTES + hb * 16384, &tmdO, &do_full[bf], 64 * hb, qi * 128, z);
-        FA_TRACE(0, it);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t id_s = idesc_bf16(128, 128, 0, 0);                 // S^T, dP^T: K-major over hd
-      const uint32_t id_kv = idesc_bf16(128, g.hd, 0, 1);               // dV, dK: A in TMEM, B MN-major
-      const uint32_t id_q0 = idesc_bf16(128, g.hd < 64 ? g.hd : 64, 1, 1);   // dQ[:, 0:64)
-      const uint32_t id_q1 = idesc_bf16(128, g.hd > 64 ? g.hd - 64 : 64, 1, 1);   // dQ[:, 64:hd)
-      const int kh = g.hd / 16;
-      mbar_wait(kv_full, 0);
-      const uint32_t aK = smem_u32(sK), aV = smem_u32(sV), adS = smem_u32(sdS);
-      for (int it = 0; it < niter; ++it) {
-        const int bf = it & 1;
-        const uint32_t aQ = smem_u32(sQ + bf * T_BYTES), adO = smem_u32(sdO + bf * T_BYTES);
-        if (it > 0) {
-          mbar_wait(tmem_free, (it - 1) & 1);                         // dQ_{i-1} read out
-          mbar_wait(&q_empty[bf ^ 1], ((it - 1) >> 1) & 1);          // P / dS of i-1 consumed by dV / dK
-        }
-        mbar_wait(&q_full[bf], (it >> 1) & 1);
-        tc_fence_after();
-        for (int k = 0; k < kh; ++k) {       // S^T = K Q^T (K-major operands over hd)
-          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
-          umma_f16(tmem + C_S, smem_desc_sw128(aK + off, 16, 1024), smem_desc_sw128(aQ + off, 16, 1024), id_s,
-                   k > 0 ? 1u : 0u);
-        }
-        mbar_wait(&do_full[bf], (it >> 1) & 1);
-        tc_fence_after();
-        for (int k = 0; k < kh; ++k) {       // dP^T = V dO^T
-          const uint32_t off = (k / 4) * 16384 + (k % 4) * 32;
-          umma_f16(tmem + C_DP, smem_desc_sw128(aV + off, 16, 1024), smem_desc_sw128(adO + off, 16, 1024), id_s,
-                   k > 0 ? 1u : 0u);
-        }
-        umma_commit(sdp_full);
-        FA_TRACE(1, it);
-        mbar_wait(ds_ready, it & 1);
-        tc_fence_after();
-        // dQ_i = dS K first (its read-out overlaps the dV / dK products); reduction over the
-        // 128 keys: MN-major views step 16 key rows = 2 KB, hd blocks 16 KB apart
-        for (int k = 0; k < 8; ++k)
-          umma_f16(tmem + C_DQ0, smem_desc_sw128(adS + k * 2048, 16384, 1024),
-                   smem_desc_sw128(aK + k * 2048, 16384, 1024), id_q0, k > 0 ? 1u : 0u);
-        if (g.hd > 64)
-          for (int k = 0; k < 8; ++k)
-            umma_f16(tmem + C_DQ1, smem_desc_sw128(adS + k * 2048, 16384, 1024),
-                     smem_desc_sw128(aK + 16384 + k * 2048, 16384, 1024), id_q1, k > 0 ? 1u : 0u);
-        umma_commit(dq_full);
-        // dV += P^T dO, dK += dS^T Q: A = the packed bf16 P^T / dS^T in TMEM (16 queries = 8 columns
-        // per step), B = dO / Q rows MN-major
-        for (int k = 0; k < 8; ++k)
-          umma_f16_ts(tmem + C_DV, tmem + C_S + 8 * k, smem_desc_sw128(adO + k * 2048, 16384, 1024), id_kv,
-                      (it > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&do_empty[bf]);
-        for (int k = 0; k < 8; ++k)
-          umma_f16_ts(tmem + C_DK, tmem + C_DP + 8 * k, smem_desc_sw128(aQ + k * 2048, 16384, 1024), id_kv,
-                      (it > 0 || k > 0) ? 1u : 0u);
-        umma_commit(&q_empty[bf]);
-        FA_TRACE(2, it);
-      }
-      umma_commit(acc_done);
-    }
-  } else {
-    const int quarter = warp % 4;
-    const int half = (warp - 2) / 4;               // query columns 64 half .. +63, dQ chunks c0 + half
-    const int r = quarter * 32 + lane;             // key row of the tile (and query row of dQ)
-    const int tq = threadIdx.x - 64;               // 0 .. 255: loader of sStat[tq]
-    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
-    const int kvrow = kt * 128 + r;
-    auto stat_load = [&](int itx) -> float {
-      const int q = (kt + it0 + itx) * 128 + (tq & 127);
-      if (q >= g.s) return 0.f;
-      return tq < 128 ? g.L2[(long long)z * g.s + q] : g.D[(long long)z * g.s + q];
-    };
-    float sn = niter > 0 ? stat_load(0) : 0.f;
-    sStat[tq] = sn;
-    if (niter > 1) sn = stat_load(1);
-    named_bar_sync(1, CW);
-    const int zb = z / g.dp.heads, zj = z % g.dp.heads;
-    for (int it = 0; it < niter; ++it) {
-      const int qi = kt + it0 + it;
-      const bool diag = qi == kt;
-      mbar_wait(sdp_full, it & 1);
-      tc_fence_after();
-      if (threadIdx.x == 64) FA_TRACE(3, it);
-      uint32_t wp[32], wd[32];
-#pragma unroll
-      for (int cc = 0; cc < 2; ++cc) {
-        const int c = 2 * half + cc;                 // 32-query chunk of the tile
-        uint32_t sv[32], dv[32];
-        tmem_ld_32x32b_x32(tmem + lane_off + C_S + 32 * c, sv);
-        tmem_ld_32x32b_x32(tmem + lane_off + C_DP + 32 * c, dv);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          float p[2], ds[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int ql = 32 * c + e + u;           // query within the tile
-            const int q = qi * 128 + ql;
-            const bool vis = q < g.s && (!diag || ql >= r);
-            const float l2 = sStat[ql], dd = sStat[128 + ql];
-            const float pr = vis ? ex2f(fmaf(__uint_as_float(sv[e + u]), g.scale_log2, -l2)) : 0.f;
-            float dpv = __uint_as_float(dv[e + u]);
-            p[u] = pr;
-            if (DROP) {   // dV uses the dropped probabilities; dP = mask * d(P_dropped)
-              const unsigned long long el = (unsigned long long)q * g.s + kvrow;
-              const bool keep = (keep4(g.dp, el / 4, g.dp.head0 + zj, g.dp.seq0 + zb) >> (el % 4)) & 1;
-              dpv = keep ? dpv * g.dp.scale : 0.f;
-              p[u] = keep ? pr * g.dp.scale : 0.f;
-            }
-            ds[u] = pr * (dpv - dd) * g.scale;
-          }
-          __nv_bfloat162 pp = __floats2bfloat162_rn(p[0], p[1]);
-          __nv_bfloat162 pd = __floats2bfloat162_rn(ds[0], ds[1]);
-          wp[16 * cc + e / 2] = *reinterpret_cast<uint32_t*>(&pp);
-          wd[16 * cc + e / 2] = *reinterpret_cast<uint32_t*>(&pd);
-        }
-      }
-      // P^T / dS^T (bf16 pairs along the query index) over S^T / dP^T: the A operands of dV / dK
-      tmem_st_32x32b_x32(tmem + lane_off + C_S + 32 * half, wp);
-      tmem_st_32x32b_x32(tmem + lane_off + C_DP + 32 * half, wd);
-      // dS^T row r (64 queries = 128 B of query block `half`) = row r of the MN-major dS operand
-      {
-        const uint32_t row = smem_u32(sdS) + half * 16384 + r * 128;
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          st_shared_v4(row + ((j ^ (r & 7)) << 4), wd[4 * j], wd[4 * j + 1], wd[4 * j + 2], wd[4 * j + 3]);
-      }
-      tmem_st_wait();
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(ds_ready);
-      if (threadIdx.x == 64) FA_TRACE(4, it);
-      // dQ_i tile -> fp32 TMA reduce-add into the dQ accumulator, staged through the dS tile
-      // (free: the dQ products that read it have completed)
-      mbar_wait(dq_full, it & 1);
-      tc_fence_after();
-      // every compute thread is past its reads of this tile's L2 / D (dq_full follows ds_ready)
-      if (it + 1 < niter) {
-        sStat[tq] = sn;
-        if (it + 2 < niter) sn = stat_load(it + 2);
-      }
-      if (threadIdx.x == 64) FA_TRACE(5, it);
-      const int nchunk = g.hd / 32;
-      const uint32_t stg = smem_u32(sdS) + half * 16384;
-      for (int c0 = 0; c0 < nchunk; c0 += 2) {
-        const int c = c0 + half;
-        const bool has = c < nchunk;                 // warp-uniform
-        uint32_t dqv[32];
-        if (has) {
-          tmem_ld_32x32b_x32(tmem + lane_off + (c < 2 ? C_DQ0 + 32 * c : C_DQ1 + 32 * (c - 2)), dqv);
-          tmem_ld_wait();
-        }
-        if (c0 + 2 >= nchunk) {
-          tc_fence_before();
-          mbar_arrive(tmem_free);      // the next S^T / dP^T products may overwrite the dQ columns
-        }
-        if (c0 >= 2) {                 // the previous boxes (same staging halves) must have been read
-          if (threadIdx.x == 64) bulk_wait_read<0>();
-          named_bar_sync(1, CW);
-        }
-        if (has) {
-          const uint32_t rowa = stg + r * 128;
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            st_shared_v4(rowa + ((j ^ (r & 7)) << 4), dqv[4 * j], dqv[4 * j + 1], dqv[4 * j + 2], dqv[4 * j + 3]);
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(1, CW);
-        if (threadIdx.x == 64) {
-          for (int u = 0; u < 2 && c0 + u < nchunk; ++u)
-            tma_reduce_add_3d(&tmdQ, sdS + u * 16384, 32 * (c0 + u), qi * 128, z);
-          bulk_commit();
-        }
-      }
-      // the dS tile is rewritten by the next iteration: wait until the TMA has read it
-      // (the barrier also publishes the next tile's L2 / D)
-      if (threadIdx.x == 64) bulk_wait_read<0>();
-      named_bar_sync(1, CW);
-      if (threadIdx.x == 64) FA_TRACE(6, it);
-    }
-    if (threadIdx.x == 64) bulk_wait_all();
-    // dK_j, dV_j rows (TMEM lane = key row) -> bf16 into the K / V slots of dQKV
-    if (niter > 0) {
-      mbar_wait(acc_done, 0);
-      tc_fence_after();
-      const bool ok = kvrow < g.s;
-      __nv_bfloat16* base = g.dQKV + (long long)kvrow * g.ldq + (long long)z * 3 * g.hd;
-      const int part = half;                            // 0: dK, 1: dV
-      const uint32_t col0 = part == 0 ? C_DK : C_DV;
-      if (g.work) {
-        // partial sums over this CTA's query tiles: fp32 reductions into the accumulators
-        float* acc = (part == 0 ? g.dKacc : g.dVacc) + ((long long)z * g.s + kvrow) * g.hd;
-        for (int c = 0; c < g.hd; c += 32) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_off + col0 + c, v);
-          tmem_ld_wait();
-          if (ok) {
-#pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4)
-              red_add_v4(acc + c + 4 * q4, __uint_as_float(v[4 * q4]), __uint_as_float(v[4 * q4 + 1]),
-                         __uint_as_float(v[4 * q4 + 2]), __uint_as_float(v[4 * q4 + 3]));
-          }
-        }
-      } else {
-        __nv_bfloat16* dst = base + (part == 0 ? g.hd : 2 * g.hd);
-        for (int c = 0; c < g.hd; c += 32) {
-          uint32_t v[32];
-          tmem_ld_32x32b_x32(tmem + lane_off + col0 + c, v);
-          tmem_ld_wait();
-          if (ok) {
-#pragma unroll
-            for (int q4 = 0; q4 < 4; ++q4) {
-              uint4 u;
-              uint32_t* w = reinterpret_cast<uint32_t*>(&u);
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                __nv_bfloat162 pr = __floats2bfloat162_rn(__uint_as_float(v[8 * q4 + 2 * e]),
-                                                          __uint_as_float(v[8 * q4 + 2 * e + 1]));
-                w[e] = *reinterpret_cast<uint32_t*>(&pr);
-              }
-              *reinterpret_cast<uint4*>(dst + c + 8 * q4) = u;
-            }
-          }
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc<fa::TMEM_COLS>(tmem);
-}
-
-namespace fab1 {  // round-1 backward (A/B reference: MP_FA_BWD_V1=1)
-// warp 0 TMA, warp 1 MMA, warps 2-9 compute: two warps per TMEM lane quarter,
-// each taking half of the 128 key columns (P / dS) and of the dQ chunks
-constexpr int THREADS = 320;
-constexpr int CW = 256;                      // compute threads
-constexpr int T_BYTES = 2 * 128 * 128;       // one [128 rows x hd<=128] bf16 tile (2 hd blocks)
-constexpr int SMEM = 6 * T_BYTES + 1024 + 512;
-}  // namespace fab1
-
-template <bool DROP>
-__global__ void __maxnreg__(168)
-flash_bwd_v1_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                 const __grid_constant__ CUtensorMap tmdQ, FabArgs g) {
-  using namespace fab1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem;
@@ -1179,22 +850,12 @@ mp_status flash_attn_bwd(const void* QKV, const void* O, const void* dO, const f
     cudaError_t e = cudaFuncSetAttribute(flash_bwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
     if (e == cudaSuccess)
       e = cudaFuncSetAttribute(flash_bwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab::SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(flash_bwd_v1_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab1::SMEM);
-    if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(flash_bwd_v1_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fab1::SMEM);
     if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention bwd smem attr: %s", cudaGetErrorString(e));
     attr = true;
   }
   const unsigned grid = work ? (unsigned)work->n : (unsigned)(zn * a.nq);
-  const bool v1 = getenv("MP_FA_BWD_V1") != nullptr;   // read per call (A/B timing)
-  if (v1) {
-    if (dp.on()) flash_bwd_v1_kernel<true><<<grid, fab1::THREADS, fab1::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
-    else flash_bwd_v1_kernel<false><<<grid, fab1::THREADS, fab1::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
-  } else {
-    if (dp.on()) flash_bwd_kernel<true><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
-    else flash_bwd_kernel<false><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
-  }
+  if (dp.on()) flash_bwd_kernel<true><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
+  else flash_bwd_kernel<false><<<grid, fab::THREADS, fab::SMEM, st>>>(tq, tk, tv, tdo, tdq, a);
   count_launch();
   {
     const long long n = zn * s * hd / 8;

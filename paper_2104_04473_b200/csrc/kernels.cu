@@ -279,13 +279,8 @@ static mp_status launch_ln_fwd(const T* in, const T* bias, const T* res, T* x1, 
 }
 
 template <class T>
-static mp_status ln_fwd_v1(int mode, bool red, const T* in, const T* bias, const T* res, T* x1, const T* g, const T* b,
-                           T* out, float* mean, float* rstd, int R, int h, float eps, Dropout dp, cudaStream_t st);
-static bool ln_v1();
-template <class T>
 mp_status layernorm_fwd(const T* x, const T* g, const T* b, T* y, float* mean, float* rstd, int R, int h, float eps,
                         cudaStream_t st) {
-  if (ln_v1()) return ln_fwd_v1<T>(0, false, x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, R, h, eps, Dropout{}, st);
   return launch_ln_fwd<T, 0, false>(x, nullptr, nullptr, nullptr, g, b, y, mean, rstd, R, h, eps, Dropout{}, st);
 }
 
@@ -293,7 +288,6 @@ template <class T>
 mp_status bda_layernorm_fwd(const T* yv, const T* bias, const T* r, T* x1, const T* g, const T* b, T* out,
                             float* mean, float* rstd, int R, int h, float eps, cudaStream_t st, Dropout dp,
                             bool red) {
-  if (ln_v1()) return ln_fwd_v1<T>(1, red, yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
   if (red) return launch_ln_fwd<T, 1, true>(yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
   return launch_ln_fwd<T, 1, false>(yv, bias, r, x1, g, b, out, mean, rstd, R, h, eps, dp, st);
 }
@@ -342,154 +336,77 @@ mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long
 }
 
 // ------------------------------------------------------------ LayerNorm bwd
-// One pass over the rows (a17): dx = rs (g dy - mean(g dy) - xhat mean(g dy xhat))
-// (+ dres), and the column sums dgamma = sum dy xhat, dbeta = sum dy, and with
-// SUMS also sum dres and sum dx (of the stored dx): the bias gradients of the
-// layer's two row-parallel outputs (b2 = colsum of the layer output gradient,
-// the residual input here; bo = colsum of dX1, the output here).  Each thread
-// keeps its columns' partials in registers over the CTA's rows; the NG groups
-// combine them in shared memory and the CTA writes one row of partials
-// part[blockIdx.x][NACC][h]; ln_part_reduce_kernel adds the column sums of part
-// into the fp32 accumulators (no global atomics, fixed summation order).
+// Two kernels: the row kernel (dx; one CTA per row, ~20 resident CTAs per SM so
+// many rows' loads are in flight) and the column-tile kernel below (dgamma,
+// dbeta and, around LN2, the two bias gradients b2 = colsum(dres) and bo =
+// colsum(dx) in the same pass over the rows).
+static int row_threads(int nvec) {
+  int t = ((nvec + 3) / 4 + 31) / 32 * 32;   // <= 4 vectors per thread
+  return std::max(32, std::min(256, t));
+}
+constexpr int LNB_MAXV = 4;
+// Grid of a row kernel: every row handled by one CTA in a grid-stride loop, the grid
+// sized to the CTAs that are resident at once (<= 64 warps / 32 CTAs per SM), so there
+// is no partial last wave (T = 4096 rows of 96 threads would be 1.3 waves).
+static int row_grid(long long R, int nvec) {
+  const int warps = row_threads(nvec) / 32;
+  const int per_sm = std::max(1, std::min(32, 64 / warps));
+  return (int)std::max(1LL, std::min<long long>(R, (long long)num_sms() * per_sm));
+}
+
+// dx: one CTA per row (fp32 block sums of dxhat and dxhat*xhat).
 // RED: dy is a multicast address (NVLS reduce-load of the TP partial sums); the
-// reduced rows are also stored to dy_copy.
-template <class T, int NV, bool RED, bool DRES, bool SUMS>
-__global__ void __launch_bounds__(ROW_THREADS) ln_bwd_kernel(const T* __restrict__ dy, const T* __restrict__ x,
-                                                      const T* __restrict__ g, const float* __restrict__ mean,
-                                                      const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                      T* __restrict__ dx, T* __restrict__ dy_copy,
-                                                      float* __restrict__ part, int h, int R, int RG, int NG) {
+// reduced rows are also stored to dy_copy for the gamma/beta kernel.
+template <class T, bool RED = false>
+__global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy, const T* __restrict__ x,
+                                                        const T* __restrict__ g, const float* __restrict__ mean,
+                                                        const float* __restrict__ rstd, const T* __restrict__ dres,
+                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy, int R) {
   constexpr int V = VW<T>::N;
-  constexpr int NACC = SUMS ? 4 : 2;
-  extern __shared__ float sacc[];   // [NACC][h]
-  __shared__ float2 red[2][ROW_MAX_NG][ROW_MAX_WARPS];
-  const int grp = threadIdx.x / RG, lt = threadIdx.x - grp * RG;
+  __shared__ float2 red[32];
   const int nvec = h / V;
-  if (NG > 1) {
-    for (int j = threadIdx.x; j < NACC * h; j += blockDim.x) sacc[j] = 0.f;
-    __syncthreads();
-  }
-  float ag[NV][V], ab[NV][V], ar[NV][V], ax[NV][V];
+  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
+  const float mu = mean[row], rs = rstd[row];
+  float xh[LNB_MAXV][V], dxh[LNB_MAXV][V];
+  float s1 = 0.f, s2 = 0.f;
 #pragma unroll
-  for (int k = 0; k < NV; ++k)
-#pragma unroll
-    for (int e = 0; e < V; ++e) { ag[k][e] = 0.f; ab[k][e] = 0.f; ar[k][e] = 0.f; ax[k][e] = 0.f; }
-  int par = 0;
-  for (long long row = (long long)blockIdx.x * NG + grp; row < R; row += (long long)gridDim.x * NG) {
-    const float mu = mean[row], rs = rstd[row];
-    float xh[NV][V], dxh[NV][V];
-    float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int vi = lt + k * RG;
-      if (vi < nvec) {
-        float d[V], xv[V], gg[V];
-        ld_in<RED>(dy + row * h + vi * V, d);
-        if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
-        ld_vec(x + row * h + vi * V, xv);
-        ld_vec(g + vi * V, gg);
-#pragma unroll
-        for (int e = 0; e < V; ++e) {
-          xh[k][e] = (xv[e] - mu) * rs;
-          dxh[k][e] = d[e] * gg[e];
-          s1 += dxh[k][e];
-          s2 += dxh[k][e] * xh[k][e];
-          ag[k][e] += d[e] * xh[k][e];
-          ab[k][e] += d[e];
-        }
-      }
-    }
-    const float2 sm = group_sum2(s1, s2, red[par][grp], lt, RG, 1 + grp);
-    par ^= 1;
-    const float m1 = sm.x / h, m2 = sm.y / h;
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int vi = lt + k * RG;
-      if (vi < nvec) {
-        float o[V];
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
-        if constexpr (DRES) {
-          float q[V];
-          ld_vec(dres + row * h + vi * V, q);
-#pragma unroll
-          for (int e = 0; e < V; ++e) {
-            o[e] += q[e];
-            if constexpr (SUMS) ar[k][e] += q[e];
-          }
-        }
-        st_vec(dx + row * h + vi * V, o);
-        if constexpr (SUMS) {
-          round_as<T>(o);   // the bias gradient sums the stored values
-#pragma unroll
-          for (int e = 0; e < V; ++e) ax[k][e] += o[e];
-        }
-      }
-    }
-  }
-  float* dst = part + (size_t)blockIdx.x * NACC * h;
-  if (NG == 1) {   // one group: its partials are the CTA's
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      const int vi = lt + k * RG;
-      if (vi < nvec) {
-#pragma unroll
-        for (int e = 0; e < V; e += 4) {
-          st_vec(dst + vi * V + e, &ag[k][e]);
-          st_vec(dst + h + vi * V + e, &ab[k][e]);
-          if constexpr (SUMS) { st_vec(dst + 2 * h + vi * V + e, &ar[k][e]); st_vec(dst + 3 * h + vi * V + e, &ax[k][e]); }
-        }
-      }
-    }
-    return;
-  }
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    const int vi = lt + k * RG;
-    if (vi < nvec)
+  for (int k = 0; k < LNB_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float d[V], xv[V], gg[V];
+      ld_in<RED>(dy + row * h + vi * V, d);
+      if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
+      ld_vec(x + row * h + vi * V, xv);
+      ld_vec(g + vi * V, gg);
 #pragma unroll
       for (int e = 0; e < V; ++e) {
-        atomicAdd(&sacc[vi * V + e], ag[k][e]);
-        atomicAdd(&sacc[h + vi * V + e], ab[k][e]);
-        if constexpr (SUMS) {
-          atomicAdd(&sacc[2 * h + vi * V + e], ar[k][e]);
-          atomicAdd(&sacc[3 * h + vi * V + e], ax[k][e]);
-        }
+        xh[k][e] = (xv[e] - mu) * rs;
+        dxh[k][e] = d[e] * gg[e];
+        s1 += dxh[k][e];
+        s2 += dxh[k][e] * xh[k][e];
       }
+    }
   }
-  __syncthreads();
-  for (int j = threadIdx.x * 4; j < NACC * h; j += blockDim.x * 4)
-    *reinterpret_cast<float4*>(dst + j) = *reinterpret_cast<const float4*>(sacc + j);
-}
-
-// out_a[n] += sum_c part[c][a][n] for the non-null outputs out_0..out_{nacc-1}.
-// CTA: 32 columns x 8 slices of the G partial rows, slices combined in shared memory.
-__global__ void __launch_bounds__(256) ln_part_reduce_kernel(const float* __restrict__ part, int G, int h, int nacc,
-                                                            float* o0, float* o1, float* o2, float* o3) {
-  __shared__ float red[8][33];
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  const int j = blockIdx.x * 32 + tx;
-  const long long ld = (long long)nacc * h;
-  float s0 = 0.f, s1 = 0.f;
-  if (j < nacc * h) {
-    int c = ty;
-    for (; c + 8 < G; c += 16) { s0 += part[c * ld + j]; s1 += part[(c + 8) * ld + j]; }
-    if (c < G) s0 += part[c * ld + j];
-  }
-  red[ty][tx] = s0 + s1;
-  __syncthreads();
-  if (ty == 0 && j < nacc * h) {
-    float s = 0.f;
+  const float2 sm = block_sum2(s1, s2, red);
+  const float m1 = sm.x / h, m2 = sm.y / h;
 #pragma unroll
-    for (int y = 0; y < 8; ++y) s += red[y][tx];
-    const int a = j / h, n = j - a * h;
-    float* o = a == 0 ? o0 : a == 1 ? o1 : a == 2 ? o2 : o3;
-    if (o) o[n] += s;
+  for (int k = 0; k < LNB_MAXV; ++k) {
+    const int vi = threadIdx.x + k * blockDim.x;
+    if (vi < nvec) {
+      float o[V];
+#pragma unroll
+      for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
+      if (dres) {
+        float q[V];
+        ld_vec(dres + row * h + vi * V, q);
+#pragma unroll
+        for (int e = 0; e < V; ++e) o[e] += q[e];
+      }
+      st_vec(dx + row * h + vi * V, o);
+    }
+  }
   }
 }
-
-// CTAs of the backward grid (and rows of partials): at most 2 per SM.
-static int ln_bwd_max_ctas() { return 2 * num_sms(); }
 
 // Column-reduction tiling shared by the bias / gamma / beta gradient kernels:
 // a CTA is CT_X column vectors x CT_Y row groups and covers CT_ROWS rows; a
@@ -583,156 +500,22 @@ mp_status dropout_colsum(const T* dY, T* dZ, float* out, int R, int N, Dropout d
   LAUNCH_CHECK();
 }
 
-// ---------------------------------------------------- round-1 row kernels
-// (A/B reference only: MP_LN_V1=1 selects them; one CTA per row, block-wide sums)
-static int row_threads_v1(int nvec) {
-  int t = ((nvec + 3) / 4 + 31) / 32 * 32;   // <= 4 vectors per thread
-  return std::max(32, std::min(256, t));
-}
-constexpr int LN_MAXV_V1 = 4;
-// Grid of a row kernel: every row handled by one CTA in a grid-stride loop, the grid
-// sized to the CTAs that are resident at once (<= 64 warps / 32 CTAs per SM), so there
-// is no partial last wave (T = 4096 rows of 96 threads would be 1.3 waves).
-static int row_grid_v1(long long R, int nvec) {
-  const int warps = row_threads_v1(nvec) / 32;
-  const int per_sm = std::max(1, std::min(32, 64 / warps));
-  return (int)std::max(1LL, std::min<long long>(R, (long long)num_sms() * per_sm));
-}
-
-// mode 0: x = in; mode 1: x = r + yv + bias (bias-dropout-add with p = 0), x1 <- x.
-template <class T, int MODE, bool RED = false>
-__global__ void __launch_bounds__(256) ln_fwd_kernel_v1(const T* __restrict__ in, const T* __restrict__ bias,
-                                                     const T* __restrict__ res, T* __restrict__ x1,
-                                                     const T* __restrict__ g, const T* __restrict__ b,
-                                                     T* __restrict__ out, float* __restrict__ mean,
-                                                     float* __restrict__ rstd, int h, float eps, Dropout dp, int R) {
-  constexpr int V = VW<T>::N;
-  __shared__ float2 red[32];
-  const int nvec = h / V;
-  // grid-stride over rows: a grid of a few resident CTAs per SM, no partial last wave
-  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
-  float v[LN_MAXV_V1][V];
-  float s1 = 0.f;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV_V1; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      ld_in<RED>(in + row * h + vi * V, v[k]);
-      if (MODE == 1) {
-        float bb[V], rr[V];
-        ld_vec(bias + vi * V, bb);
-        ld_vec(res + row * h + vi * V, rr);
-        if (dp.on()) {   // x1 = r + dropout(y + bias), mask keyed by (sequence, position, feature)
-          const int pos = (int)(row / dp.b), seq = dp.seq0 + (int)(row % dp.b);
-          const uint32_t km = keep_bits<V>(dp, (unsigned long long)pos * h + vi * V, 0, seq);
-#pragma unroll
-          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + ((km >> e) & 1 ? (v[k][e] + bb[e]) * dp.scale : 0.f);
-        } else {
-#pragma unroll
-          for (int e = 0; e < V; ++e) v[k][e] = rr[e] + (v[k][e] + bb[e]);
-        }
-        st_vec(x1 + row * h + vi * V, v[k]);
-        // LayerNorm consumes the stored (rounded) residual stream value
-        ld_vec(x1 + row * h + vi * V, v[k]);
-      }
-#pragma unroll
-      for (int e = 0; e < V; ++e) s1 += v[k][e];
-    }
-  }
-  const float mu = block_sum2(s1, 0.f, red).x / h;
-  float s2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV_V1; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec)
-#pragma unroll
-      for (int e = 0; e < V; ++e) { float d = v[k][e] - mu; s2 += d * d; }
-  }
-  const float var = block_sum2(s2, 0.f, red).x / h;
-  const float rs = rsqrtf(var + eps);
-#pragma unroll
-  for (int k = 0; k < LN_MAXV_V1; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      float gg[V], bb[V], o[V];
-      ld_vec(g + vi * V, gg);
-      ld_vec(b + vi * V, bb);
-#pragma unroll
-      for (int e = 0; e < V; ++e) o[e] = (v[k][e] - mu) * rs * gg[e] + bb[e];
-      st_vec(out + row * h + vi * V, o);
-    }
-  }
-  if (threadIdx.x == 0) { mean[row] = mu; rstd[row] = rs; }
-  }
-}
-
-// dx: one CTA per row (fp32 block sums of dxhat and dxhat*xhat).
-// RED: dy is a multicast address (NVLS reduce-load of the TP partial sums); the
-// reduced rows are also stored to dy_copy for the gamma/beta kernel.
-template <class T, bool RED = false>
-__global__ void __launch_bounds__(256) ln_bwd_dx_kernel_v1(const T* __restrict__ dy, const T* __restrict__ x,
-                                                        const T* __restrict__ g, const float* __restrict__ mean,
-                                                        const float* __restrict__ rstd, const T* __restrict__ dres,
-                                                        T* __restrict__ dx, int h, T* __restrict__ dy_copy, int R) {
-  constexpr int V = VW<T>::N;
-  __shared__ float2 red[32];
-  const int nvec = h / V;
-  for (long long row = blockIdx.x; row < R; row += gridDim.x) {
-  const float mu = mean[row], rs = rstd[row];
-  float xh[LN_MAXV_V1][V], dxh[LN_MAXV_V1][V];
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV_V1; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      float d[V], xv[V], gg[V];
-      ld_in<RED>(dy + row * h + vi * V, d);
-      if constexpr (RED) st_vec(dy_copy + row * h + vi * V, d);
-      ld_vec(x + row * h + vi * V, xv);
-      ld_vec(g + vi * V, gg);
-#pragma unroll
-      for (int e = 0; e < V; ++e) {
-        xh[k][e] = (xv[e] - mu) * rs;
-        dxh[k][e] = d[e] * gg[e];
-        s1 += dxh[k][e];
-        s2 += dxh[k][e] * xh[k][e];
-      }
-    }
-  }
-  const float2 sm = block_sum2(s1, s2, red);
-  const float m1 = sm.x / h, m2 = sm.y / h;
-#pragma unroll
-  for (int k = 0; k < LN_MAXV_V1; ++k) {
-    const int vi = threadIdx.x + k * blockDim.x;
-    if (vi < nvec) {
-      float o[V];
-#pragma unroll
-      for (int e = 0; e < V; ++e) o[e] = rs * (dxh[k][e] - m1 - xh[k][e] * m2);
-      if (dres) {
-        float q[V];
-        ld_vec(dres + row * h + vi * V, q);
-#pragma unroll
-        for (int e = 0; e < V; ++e) o[e] += q[e];
-      }
-      st_vec(dx + row * h + vi * V, o);
-    }
-  }
-  }
-}
-
-// dgamma[n] += sum_r dy[r,n] (x[r,n] - mean[r]) rstd[r];  dbeta[n] += sum_r dy[r,n]
-template <class T>
-__global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel_v1(const T* __restrict__ dy, const T* __restrict__ x,
+// dgamma[n] += sum_r dy[r,n] (x[r,n] - mean[r]) rstd[r];  dbeta[n] += sum_r dy[r,n];
+// SUMS: also dres_sum[n] += sum_r dres[r,n], dx_sum[n] += sum_r dx[r,n] (stored values)
+template <class T, bool SUMS>
+__global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel(const T* __restrict__ dy, const T* __restrict__ x,
                                                                const float* __restrict__ mean,
                                                                const float* __restrict__ rstd,
+                                                               const T* __restrict__ dres, const T* __restrict__ dx,
                                                                float* __restrict__ dgamma, float* __restrict__ dbeta,
+                                                               float* __restrict__ dres_sum, float* __restrict__ dx_sum,
                                                                int R, int h) {
   constexpr int V = VW<T>::N;
   __shared__ float red[CT_Y * CT_X * V];
   const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
   const int nv = h / V, vi = blockIdx.x * CT_X + tx;
   const int r0 = blockIdx.y * CT_ROWS, r1 = min(R, r0 + CT_ROWS);
-  float ag[V] = {}, ab[V] = {};
+  float ag[V] = {}, ab[V] = {}, ar[V] = {}, ax[V] = {};
   if (vi < nv) {
 #pragma unroll 4
     for (int r = r0 + ty; r < r1; r += CT_Y) {
@@ -745,108 +528,48 @@ __global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel_v1(const T* __re
         ag[e] += d[e] * (xv[e] - mu) * rs;
         ab[e] += d[e];
       }
+      if constexpr (SUMS) {
+        float q[V], o[V];
+        ld_vec(dres + (long long)r * h + vi * V, q);
+        ld_vec(dx + (long long)r * h + vi * V, o);
+#pragma unroll
+        for (int e = 0; e < V; ++e) { ar[e] += q[e]; ax[e] += o[e]; }
+      }
     }
   }
   ct_reduce_add<V>(ag, red, dgamma, vi, nv);
   __syncthreads();
   ct_reduce_add<V>(ab, red, dbeta, vi, nv);
-}
-
-
-template <class T>
-static mp_status ln_fwd_v1(int mode, bool red, const T* in, const T* bias, const T* res, T* x1, const T* g, const T* b,
-                           T* out, float* mean, float* rstd, int R, int h, float eps, Dropout dp, cudaStream_t st) {
-  const int nv = h / VW<T>::N;
-  if (mode == 0)
-    ln_fwd_kernel_v1<T, 0><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(in, nullptr, nullptr, nullptr, g, b, out, mean, rstd, h, eps, Dropout{}, R);
-  else if (red)
-    ln_fwd_kernel_v1<T, 1, true><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R);
-  else
-    ln_fwd_kernel_v1<T, 1><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R);
-  LAUNCH_CHECK();
-}
-template <class T>
-mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st);
-template <class T>
-static mp_status ln_bwd_v1(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
-                           T* dx, float* dgamma, float* dbeta, int R, int h, cudaStream_t st, T* dy_copy,
-                           float* dres_sum, float* dx_sum) {
-  const int nv = h / VW<T>::N;
-  if (dy_copy) {
-    ln_bwd_dx_kernel_v1<T, true><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, dy_copy, R);
-    dy = dy_copy;
-  } else {
-    ln_bwd_dx_kernel_v1<T><<<row_grid_v1(R, nv), row_threads_v1(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, nullptr, R);
+  if constexpr (SUMS) {
+    __syncthreads();
+    if (dres_sum) ct_reduce_add<V>(ar, red, dres_sum, vi, nv);
+    __syncthreads();
+    if (dx_sum) ct_reduce_add<V>(ax, red, dx_sum, vi, nv);
   }
-  count_launch();
-  ln_bwd_gb_kernel_v1<T><<<ct_grid(h / VW<T>::N, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dgamma, dbeta, R, h);
-  count_launch();
-  if (dres_sum) MP_TRY(colsum_accum<T>(dres, dres_sum, R, h, st));
-  if (dx_sum) MP_TRY(colsum_accum<T>(dx, dx_sum, R, h, st));
-  return MP_OK;
-}
-static bool ln_v1() { return getenv("MP_LN_V1") != nullptr; }
-
-template <class T, int NV, bool RED, bool DRES, bool SUMS>
-static void launch_ln_bwd(const RowCfg& rc, const T* dy, const T* x, const T* g, const float* mean,
-                          const float* rstd, const T* dres, T* dx, T* dy_copy, float* part, int h, int R,
-                          cudaStream_t st, int* grid_out) {
-  auto kern = ln_bwd_kernel<T, NV, RED, DRES, SUMS>;
-  const int threads = rc.RG * rc.NG;
-  const size_t smem = rc.NG > 1 ? sizeof(float) * (SUMS ? 4 : 2) * h : 0;
-  static int attr_set = -1;   // dynamic shared memory above 48 KB needs the opt-in (h up to 16384)
-  if (smem > 48 * 1024 && attr_set < (int)smem) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = (int)smem;
-  }
-  const long long need = (R + rc.NG - 1) / rc.NG;
-  const int occ = std::min(2, resident_ctas(kern, threads, smem));
-  const int grid = (int)std::min<long long>(need, std::min<long long>(ln_bwd_max_ctas(), (long long)num_sms() * occ));
-  kern<<<grid, threads, smem, st>>>(dy, x, g, mean, rstd, dres, dx, dy_copy, part, h, R, rc.RG, rc.NG);
-  *grid_out = grid;
-}
-
-template <class T, bool RED, bool DRES, bool SUMS>
-static void ln_bwd_nv(const RowCfg& rc, const T* dy, const T* x, const T* g, const float* mean, const float* rstd,
-                      const T* dres, T* dx, T* dy_copy, float* part, int h, int R, cudaStream_t st, int* grid) {
-#define LNB_NV(NV) launch_ln_bwd<T, NV, RED, DRES, SUMS>(rc, dy, x, g, mean, rstd, dres, dx, dy_copy, part, h, R, st, grid)
-  switch (rc.NV) {
-    case 1: LNB_NV(1); break;
-    case 2: LNB_NV(2); break;
-    case 3: LNB_NV(3); break;
-    case 4: LNB_NV(4); break;
-    default: LNB_NV(8); break;
-  }
-#undef LNB_NV
-}
-
-long long layernorm_bwd_scratch_floats(int R, int h) {
-  (void)R;
-  return (long long)ln_bwd_max_ctas() * 4 * h;
 }
 
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
-                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st,
-                        T* dy_copy, float* dres_sum, float* dx_sum) {
+                        T* dx, float* dgamma, float* dbeta, int R, int h, cudaStream_t st, T* dy_copy,
+                        float* dres_sum, float* dx_sum) {
   MP_TRY(check_row_dims<T>(R, h));
-  if (!scratch) return set_err(MP_EINVAL, "layernorm_bwd: scratch of layernorm_bwd_scratch_floats() floats required");
   if ((dres_sum || dx_sum) && !dres) return set_err(MP_EINVAL, "layernorm_bwd: column sums need dres");
-  if (ln_v1()) return ln_bwd_v1<T>(dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, R, h, st, dy_copy, dres_sum, dx_sum);
-  const RowCfg rc = row_cfg<T>(h);
-  const bool sums = dres_sum || dx_sum;
-  int grid = 0;
-  // dispatch on (RED, DRES, SUMS); SUMS implies DRES
-#define LNB(RED, DRES, SUMS) ln_bwd_nv<T, RED, DRES, SUMS>(rc, dy, x, g, mean, rstd, dres, dx, dy_copy, scratch, h, R, st, &grid)
+  const int nv = h / VW<T>::N;
+  if (nv > LNB_MAXV * 256) return set_err(MP_EINVAL, "layernorm_bwd: h=%d too large", h);
   if (dy_copy) {
-    if (sums) LNB(true, true, true); else if (dres) LNB(true, true, false); else LNB(true, false, false);
+    ln_bwd_dx_kernel<T, true><<<row_grid(R, nv), row_threads(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h,
+                                                                            dy_copy, R);
+    dy = dy_copy;
   } else {
-    if (sums) LNB(false, true, true); else if (dres) LNB(false, true, false); else LNB(false, false, false);
+    ln_bwd_dx_kernel<T><<<row_grid(R, nv), row_threads(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, nullptr, R);
   }
-#undef LNB
   count_launch();
-  const int nacc = sums ? 4 : 2;
-  ln_part_reduce_kernel<<<(nacc * h + 31) / 32, 256, 0, st>>>(scratch, grid, h, nacc, dgamma, dbeta, dres_sum, dx_sum);
+  if (dres_sum || dx_sum)
+    ln_bwd_gb_kernel<T, true><<<ct_grid(nv, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dres, dx, dgamma, dbeta,
+                                                                      dres_sum, dx_sum, R, h);
+  else
+    ln_bwd_gb_kernel<T, false><<<ct_grid(nv, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, nullptr, nullptr, dgamma,
+                                                                       dbeta, nullptr, nullptr, R, h);
   LAUNCH_CHECK();
 }
 
@@ -1399,7 +1122,7 @@ mp_status cast_from_f32(const float* src, T* dst, long long n, cudaStream_t st) 
   template mp_status dropout_colsum<T>(const T*, T*, float*, int, int, Dropout, cudaStream_t);                      \
   template mp_status attn_dropout<T>(const T*, T*, long long, int, Dropout, cudaStream_t);                          \
   template mp_status layernorm_bwd<T>(const T*, const T*, const T*, const float*, const float*, const T*, T*,        \
-                                      float*, float*, float*, int, int, cudaStream_t, T*, float*, float*);          \
+                                      float*, float*, int, int, cudaStream_t, T*, float*, float*);                  \
   template mp_status bias_gelu_fwd<T>(const T*, const T*, T*, long long, int, cudaStream_t);                         \
   template mp_status bias_gelu_bwd<T>(const T*, const T*, const T*, T*, float*, int, int, cudaStream_t);             \
   template mp_status colsum_accum<T>(const T*, float*, int, int, cudaStream_t);                                     \

@@ -38,17 +38,15 @@ mp_status dropout_colsum(const T* dY, T* dZ, float* db, int R, int N, Dropout dp
 // Pd = dropout(P) over the causal written region (unfused attention dropout)
 template <class T>
 mp_status attn_dropout(const T* P, T* Pd, long long z, int s, Dropout dp, cudaStream_t st);
-// dx = LN backward of dy (+ dres if non-null); dgamma/dbeta accumulated (fp32, +=), one pass.
+// dx = LN backward of dy (+ dres if non-null); dgamma/dbeta accumulated (fp32, +=).
 // dy_copy non-null: dy is a multicast address, dy = NVLS reduce-load of the t
 // partials (the f all-reduce fused into the load), stored to dy_copy [R, h].
-// scratch: layernorm_bwd_scratch_floats(R, h) floats (per-CTA column partials).
 // dres_sum / dx_sum (optional, need dres): += column sums of dres and of the
 // stored dx (the bias gradients of the row-parallel outputs around LN2, a17).
 template <class T>
 mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, const float* rstd, const T* dres,
-                        T* dx, float* dgamma, float* dbeta, float* scratch, int R, int h, cudaStream_t st,
+                        T* dx, float* dgamma, float* dbeta, int R, int h, cudaStream_t st,
                         T* dy_copy = nullptr, float* dres_sum = nullptr, float* dx_sum = nullptr);
-long long layernorm_bwd_scratch_floats(int R, int h);
 // H = gelu(Y + b)
 template <class T>
 mp_status bias_gelu_fwd(const T* yv, const T* b, T* out, long long R, int N, cudaStream_t st);

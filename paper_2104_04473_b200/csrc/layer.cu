@@ -154,7 +154,6 @@ mp_status ensure_workspace(mp_ctx* c, int b) {
   void** bufs[] = {&c->ws_z, &c->ws_dsq, &c->ws_d4h, &c->ws_dh1, &c->ws_dh2, &c->ws_dqkv, &c->ws_dctx};
   for (void** q : bufs)
     if (*q) { cudaFree(*q); *q = nullptr; }
-  if (c->ws_ln) { cudaFree(c->ws_ln); c->ws_ln = nullptr; }
   if (c->ws_fa) { cudaFree(c->ws_fa); c->ws_fa = nullptr; }
   Dims d = dims(c, b);
   const bool fused = use_fused(c);
@@ -163,7 +162,6 @@ mp_status ensure_workspace(mp_ctx* c, int b) {
                     (size_t)d.T * d.h * es, (size_t)d.T * d.h * es, (size_t)d.T * d.h3t * es,
                     (size_t)d.T * d.ht * es};
   for (int i = 0; i < 7; ++i) MP_CUDA(cudaMalloc(bufs[i], al256(sizes[i])));
-  MP_CUDA(cudaMalloc(&c->ws_ln, al256(sizeof(float) * std::max(1LL, layernorm_bwd_scratch_floats(d.T, d.h)))));
   if (fused) MP_CUDA(cudaMalloc(&c->ws_fa, al256(sizeof(float) * (size_t)flash_bwd_ws_floats(d.s, d.b, d.heads, d.hd))));
   c->ws_b = b;
   return MP_OK;
@@ -379,7 +377,7 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   }
   // dX1 = LN2'(dA2) + dY, with db2 = colsum(dY) and dbo = colsum(dX1) (no dropout) in the same pass
   MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.X1, ptr<T>(c, lp[P_LN2G]), st.mu2, st.rs2, dY, dX1,
-                          gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), c->ws_ln, d.T, d.h, c->cs,
+                          gptr(c, lp[P_LN2G]), gptr(c, lp[P_LN2B]), d.T, d.h, c->cs,
                           nvr ? dA2 : nullptr, dp2.on() ? nullptr : gptr(c, lp[P_B2]),
                           dp1.on() ? nullptr : gptr(c, lp[P_BO])));
   // attention block: dZ1 = dropout mask * dX1; dbo; dctx = dZ1 Wo; dWo += ctx^T dZ1
@@ -422,7 +420,7 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
     MP_TRY(lin_wgrad(c, c->ws_dqkv, st.A, gptr(c, lp[P_WQKV]), d.T, d.h3t, d.h));
   }
   MP_TRY(layernorm_bwd<T>((const T*)fr, (const T*)st.x, ptr<T>(c, lp[P_LN1G]), st.mu1, st.rs1, dX1, (T*)dx,
-                          gptr(c, lp[P_LN1G]), gptr(c, lp[P_LN1B]), c->ws_ln, d.T, d.h, c->cs,
+                          gptr(c, lp[P_LN1G]), gptr(c, lp[P_LN1B]), d.T, d.h, c->cs,
                           nvr ? dA : nullptr));
   if (nv) MP_CUDA(cudaStreamWaitEvent(c->cs, ev_b, 0));   // dWqkv done before the stash is released
   return MP_OK;
@@ -530,7 +528,7 @@ static mp_status head_bf16(mp_ctx* c, const void* X, const int* dlab, int lab_ld
     MP_TRY(gemm(c->cfg.dtype, g, c->cs));
   }
   MP_TRY(layernorm_bwd<T>(dZ, (const T*)X, ptr<T>(c, ig), mu, rs, nullptr, (T*)dX,
-                          gptr(c, ig), gptr(c, ib), c->ws_ln, Tn, h, c->cs));
+                          gptr(c, ig), gptr(c, ib), Tn, h, c->cs));
   MP_CUDA(cudaFreeAsync(blk, c->cs));
   return MP_OK;
 }
@@ -595,7 +593,7 @@ static mp_status head_t(mp_ctx* c, const void* X, const int* dlab, int lab_ld, i
     MP_TRY(gemm(c->cfg.dtype, g, c->cs));
   }
   MP_TRY(layernorm_bwd<T>(dZ, (const T*)X, ptr<T>(c, ig), mu, rs, nullptr, (T*)dX,
-                          gptr(c, ig), gptr(c, ib), c->ws_ln, Tn, h, c->cs));
+                          gptr(c, ig), gptr(c, ib), Tn, h, c->cs));
   MP_CUDA(cudaFreeAsync(blk, c->cs));
   return MP_OK;
 }

@@ -32,10 +32,10 @@ static mp_status bda_ln_(const void* y, const void* bias, const void* r, void* x
 }
 template <class T>
 static mp_status ln_bwd_(const void* dy, const void* x, const void* g, const float* mu, const float* rs,
-                         const void* dres, void* dx, float* dg, float* db, float* dres_sum, float* dx_sum,
-                         float* scratch, int R, int h, cudaStream_t st) {
-  return layernorm_bwd<T>(C<T>(dy), C<T>(x), C<T>(g), mu, rs, C<T>(dres), M<T>(dx), dg, db, scratch, R, h, st,
-                          nullptr, dres_sum, dx_sum);
+                         const void* dres, void* dx, float* dg, float* db, float* dres_sum, float* dx_sum, int R,
+                         int h, cudaStream_t st) {
+  return layernorm_bwd<T>(C<T>(dy), C<T>(x), C<T>(g), mu, rs, C<T>(dres), M<T>(dx), dg, db, R, h, st, nullptr,
+                          dres_sum, dx_sum);
 }
 template <class T>
 static mp_status gelu_fwd_(const void* y, const void* b, void* out, long long R, int N, cudaStream_t st) {
@@ -73,20 +73,15 @@ mp_status mp_op_bda_layernorm_fwd(mp_dtype dt, const void* y, const void* bias, 
 }
 
 mp_status mp_op_layernorm_bwd(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
-                              const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
-                              float* scratch, int R, int h, void* stream) {
-  DISPATCH(dt, ln_bwd_, (dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, nullptr, nullptr, scratch, R, h, _st));
+                              const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta, int R, int h,
+                              void* stream) {
+  DISPATCH(dt, ln_bwd_, (dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, nullptr, nullptr, R, h, _st));
 }
 
 mp_status mp_op_layernorm_bwd_sums(mp_dtype dt, const void* dy, const void* x, const void* g, const float* mean,
                                    const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
-                                   float* dres_sum, float* dx_sum, float* scratch, int R, int h, void* stream) {
-  DISPATCH(dt, ln_bwd_, (dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, dres_sum, dx_sum, scratch, R, h, _st));
-}
-
-long long mp_op_layernorm_bwd_scratch_floats(int R, int h) {
-  if (mp::require_device() != MP_OK) return 0;
-  return mp::layernorm_bwd_scratch_floats(R, h);
+                                   float* dres_sum, float* dx_sum, int R, int h, void* stream) {
+  DISPATCH(dt, ln_bwd_, (dy, x, g, mean, rstd, dres, dx, dgamma, dbeta, dres_sum, dx_sum, R, h, _st));
 }
 
 mp_status mp_op_bias_gelu_fwd(mp_dtype dt, const void* y, const void* b, void* out, long long R, int N,

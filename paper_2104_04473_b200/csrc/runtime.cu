@@ -291,7 +291,7 @@ mp_status mp_finalize(mp_ctx* c) {
   ncclComm_t comms[] = {c->tp_comm, c->emb_comm, c->dp_comm, c->world_comm};
   for (auto cm : comms)
     if (cm) ncclCommDestroy(cm);
-  void* bufs[] = {c->ws_z, c->ws_dsq, c->ws_d4h, c->ws_dh1, c->ws_dh2, c->ws_dqkv, c->ws_dctx, c->ws_ln, c->ws_fa,
+  void* bufs[] = {c->ws_z, c->ws_dsq, c->ws_d4h, c->ws_dh1, c->ws_dh2, c->ws_dqkv, c->ws_dctx, c->ws_fa,
                   c->grads, c->adam_m, c->adam_v, c->d_loss, c->master, c->head_dl, c->head_z};
   for (void* q : bufs)
     if (q) cudaFree(q);

@@ -84,7 +84,6 @@ struct mp_ctx {
   int ws_b = 0;
   void *ws_z = nullptr, *ws_dsq = nullptr, *ws_d4h = nullptr, *ws_dh1 = nullptr, *ws_dh2 = nullptr,
        *ws_dqkv = nullptr, *ws_dctx = nullptr;
-  float* ws_ln = nullptr;
   float* ws_fa = nullptr;          // fused-attention backward workspace (dQ accumulator, D)
   float* d_loss = nullptr;
   // deferred logit-layer weight gradient (bf16, last stage): every microbatch's dlogits and

@@ -102,9 +102,8 @@ SIGNATURES = {
     "mp_op_gemm_config": (_I, [ctypes.POINTER(GemmDesc), _P]),
     "mp_op_layernorm_fwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P]),
     "mp_op_bda_layernorm_fwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _F, _P]),
-    "mp_op_layernorm_bwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
-    "mp_op_layernorm_bwd_sums": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
-    "mp_op_layernorm_bwd_scratch_floats": (_LL, [_I, _I]),
+    "mp_op_layernorm_bwd": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
+    "mp_op_layernorm_bwd_sums": (_I, [_I, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _I, _I, _P]),
     "mp_op_bias_gelu_fwd": (_I, [_I, _P, _P, _P, _LL, _I, _P]),
     "mp_op_bias_gelu_bwd": (_I, [_I, _P, _P, _P, _P, _P, _I, _I, _P]),
     "mp_op_softmax_causal_fwd": (_I, [_I, _P, _LL, _I, _F, _P]),

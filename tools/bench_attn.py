@@ -6,8 +6,7 @@ Shapes (s = 2048): the per-rank attention of the BASELINE configs --
 1.7B b=2 t=1 (48 heads x hd 96), 1.7B b=2 t=2 (24 x 96), 18.4B b=1 t=2
 (24 x 128), 39.1B b=1 t=2 (32 x 128).  Reports fwd and bwd (incl. the D /
 dQ-convert helpers) in us and TFLOP/s of causal-algorithmic work:
-fwd 2 products, bwd 5 products, each 2 hd s(s+1)/2 per head.  --ab also
-times the round-1 backward (MP_FA_BWD_V1=1) on the same buffers.
+fwd 2 products, bwd 5 products, each 2 hd s(s+1)/2 per head.
 """
 import argparse
 import json
@@ -39,7 +38,6 @@ def timeit(fn, reps):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--reps", type=int, default=20)
-    ap.add_argument("--ab", action="store_true")
     args = ap.parse_args()
     mp.lib()
     shapes = [("1.7B b2 t1", 2048, 2, 24, 96), ("1.7B b2 t2", 2048, 2, 12, 96), ("18.4B b1 t2", 2048, 1, 24, 128),
@@ -62,13 +60,6 @@ def main():
         rec = {"shape": name, "s": s, "b": b, "heads": heads, "hd": hd, "fwd_us": round(tf, 1),
                "fwd_tflops": round(2 * prod / tf / 1e6, 1), "bwd_us": round(tb, 1),
                "bwd_tflops": round(5 * prod / tb / 1e6, 1)}
-        if args.ab:
-            ref = dq.clone()
-            os.environ["MP_FA_BWD_V1"] = "1"
-            t1 = timeit(bwd, args.reps)
-            del os.environ["MP_FA_BWD_V1"]
-            rec["bwd_v1_us"] = round(t1, 1)
-            rec["max_abs_diff_vs_v1"] = float((dq.float() - ref.float()).abs().max())
         print(json.dumps(rec), flush=True)
 
 

@@ -57,7 +57,6 @@ def main():
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--R", type=int, default=4096)
     ap.add_argument("--widths", default="2304,4096,6144,8192")
-    ap.add_argument("--ab", action="store_true", help="also time the round-1 kernels (MP_LN_V1=1)")
     args = ap.parse_args()
     mp.lib()
     peak = None
@@ -75,7 +74,6 @@ def main():
         b = (0.1 * torch.randn(h, device="cuda")).to(bf)
         mu, rs = (torch.empty(R, device="cuda") for _ in range(2))
         acc = torch.zeros(4, h, device="cuda")
-        scratch = torch.empty(max(1, mp.raw("mp_op_layernorm_bwd_scratch_floats", R, h)), device="cuda")
         st = torch.cuda.current_stream().cuda_stream
         E = 2 * R * h
         kernels = {
@@ -86,20 +84,18 @@ def main():
                                            rs.data_ptr(), R, h, 1e-5, st), 4 * E + 8 * R),
             "ln_bwd": (lambda: mp.call("mp_op_layernorm_bwd", "bf16", dy.data_ptr(), x.data_ptr(), g.data_ptr(),
                                        mu.data_ptr(), rs.data_ptr(), dres.data_ptr(), dx.data_ptr(),
-                                       acc[0].data_ptr(), acc[1].data_ptr(), scratch.data_ptr(), R, h, st),
+                                       acc[0].data_ptr(), acc[1].data_ptr(), R, h, st),
                        4 * E + 8 * R),
             "ln_bwd_sums": (lambda: mp.call("mp_op_layernorm_bwd_sums", "bf16", dy.data_ptr(), x.data_ptr(),
                                             g.data_ptr(), mu.data_ptr(), rs.data_ptr(), dres.data_ptr(),
                                             dx.data_ptr(), acc[0].data_ptr(), acc[1].data_ptr(), acc[2].data_ptr(),
-                                            acc[3].data_ptr(), scratch.data_ptr(), R, h, st), 4 * E + 8 * R),
+                                            acc[3].data_ptr(), R, h, st), 4 * E + 8 * R),
             "colsum": (lambda: mp.call("mp_op_colsum_accum", "bf16", dy.data_ptr(), acc[0].data_ptr(), R, h, st),
                        E),
         }
         mp.call("mp_op_layernorm_fwd", "bf16", x.data_ptr(), g.data_ptr(), b.data_ptr(), o.data_ptr(),
                 mu.data_ptr(), rs.data_ptr(), R, h, 1e-5, st)
-        for variant in (["new", "v1"] if args.ab else ["new"]):
-            if variant == "v1":
-                os.environ["MP_LN_V1"] = "1"
+        for variant in ["current"]:
             for name, (fn, nbytes) in kernels.items():
                 warm = timeit(fn, args.reps)
                 cold = timeit(fn, args.reps, flush)
@@ -110,7 +106,6 @@ def main():
                     rec["cold_frac"] = round(nbytes / cold / 1e3 / peak, 3)
                 out.append(rec)
                 print(json.dumps(rec), flush=True)
-            os.environ.pop("MP_LN_V1", None)
 
 
 if __name__ == "__main__":
