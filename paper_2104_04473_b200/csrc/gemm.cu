@@ -29,6 +29,7 @@
 #include "common.h"
 #include "tma_host.h"
 #include "gemm.h"
+#include "launch.cuh"
 #include "../../include/mp_ops.h"
 
 namespace mp {
@@ -67,6 +68,7 @@ struct TcArgs {
   float* colsum;        // act 2: colsum[n] += sum_m C[m, n] (optional)
   int pair;             // CTA-pair kernel: m_blocks count 256-row pair tiles
   int kb_per_tile;      // k-blocks per tile (stream_k)
+  int sk_first;         // stream_k: tiles [0, sk_first) run whole (full waves), the rest is split
   float alpha;
   // act 3 (logit layer + cross-entropy statistics, a18 / P:577): besides the bf16
   // logits, per (row, n-block, epilogue half) the fp32 max and sum of exp(x - max)
@@ -107,10 +109,12 @@ __device__ __forceinline__ float dgelu_fast(float u) {
 // Work sequence of one CTA, identical for the producer, MMA and epilogue roles.
 // Tile mode: tiles blockIdx.x, +gridDim.x, ... with their (causal) k-block ranges.
 // Stream-K mode (accumulate GEMMs, whose epilogue is a TMA reduce-add into the
-// fp32 accumulator): the num_tiles * kb_per_tile (tile, k-block) iterations are
-// cut into gridDim.x equal contiguous ranges, so every SM gets the same number
-// of k-blocks (no partial last wave); a tile split between CTAs is simply
-// reduce-added twice.
+// fp32 accumulator): the tiles of the full waves [0, sk_first) run whole in tile
+// order (concurrent CTAs work on neighbouring tiles, so operand panels are
+// shared in L2 at the same k position), then the remaining tiles' (tile,
+// k-block) iterations are cut into gridDim.x equal contiguous ranges, so every
+// SM gets the same number of k-blocks (no partial last wave); a tile split
+// between CTAs is simply reduce-added twice.
 struct WorkIter {
   long long i, i1;
   int t, nb;
@@ -119,15 +123,23 @@ struct WorkIter {
     const int b = g.pair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
     nb = g.pair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
     if (g.stream_k) {
-      const long long I = (long long)g.num_tiles * g.kb_per_tile;
-      i = I * b / nb;
-      i1 = I * (b + 1) / nb;
+      const long long I = (long long)(g.num_tiles - g.sk_first) * g.kb_per_tile;
+      const long long i0 = (long long)g.sk_first * g.kb_per_tile;
+      i = i0 + I * b / nb;
+      i1 = i0 + I * (b + 1) / nb;
     }
     t = b;
   }
   template <int BN>
   __device__ __forceinline__ bool next(const TcArgs& g, int& tile, int& kb0, int& kb1) {
     if (g.stream_k) {
+      if (t < g.sk_first) {   // full waves: whole tiles
+        tile = t;
+        t += nb;
+        kb0 = 0;
+        kb1 = g.kb_per_tile;
+        return true;
+      }
       if (i >= i1) return false;
       tile = (int)(i / g.kb_per_tile);
       kb0 = (int)(i % g.kb_per_tile);
@@ -197,6 +209,7 @@ tc_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const int tiles_per_batch = g.m_blocks * g.n_blocks;
+  pdl_entry();   // the prologue above overlaps the previous kernel's tail
 
   if (warp == 0) {
     if (lane == 0) {
@@ -545,6 +558,7 @@ constexpr int SB_M = 64, SB_N = 64, SB_K = 16;
 
 __global__ void __launch_bounds__(256)
 simt_gemm_kernel(mp_gemm_desc g, int m_blocks, int n_blocks) {
+  pdl_entry();
   __shared__ float As[SB_K][SB_M + 4];
   __shared__ float Bs[SB_K][SB_N + 4];
   const int z = blockIdx.z;
@@ -660,16 +674,18 @@ static cudaError_t launch_tc(const CUtensorMap& ta, const CUtensorMap& tb, const
     cfg.blockDim = dim3(GEMM_THREADS);
     cfg.dynamicSmemBytes = Cfg::SMEM;
     cfg.stream = st;
-    cudaLaunchAttribute attrs[1];
+    cudaLaunchAttribute attrs[2];
     attrs[0].id = cudaLaunchAttributeClusterDimension;
     attrs[0].val.clusterDim.x = 2;
     attrs[0].val.clusterDim.y = 1;
     attrs[0].val.clusterDim.z = 1;
+    attrs[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = attrs;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     return cudaLaunchKernelEx(&cfg, k, ta, tb, tc, tc2, a);
   } else {
-    k<<<grid, GEMM_THREADS, Cfg::SMEM, st>>>(ta, tb, tc, tc2, a);
+    pdl_launch(k, grid, GEMM_THREADS, Cfg::SMEM, st, ta, tb, tc, tc2, a);
     return cudaGetLastError();
   }
 }
@@ -753,14 +769,6 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st, const GemmCe* ce = n
       return set_err(MP_EINVAL, "gemm: act needs bf16 C / C2, 16-byte aligned, no accumulate");
   }
   a.kb_per_tile = (g.K + BK - 1) / BK;
-  // Raster: by default consecutive tiles share the B panel (m fastest).  When A
-  // is the large operand and B fits comfortably in L2 (e.g. the logit-layer
-  // weight gradient dE = dlogits^T Z, A = 210 MB, B = 9 MB), walk n fastest so
-  // every A panel is streamed from DRAM once instead of once per n-block.
-  {
-    const double a_bytes = 2.0 * g.M * (double)g.K * g.batch, b_bytes = 2.0 * g.N * (double)g.K * g.batch;
-    a.n_fast = (a.n_blocks > 1 && a_bytes > 2.0 * b_bytes && b_bytes < 32e6) ? 1 : 0;
-  }
   // CTA pairs (cta_group::2, 256 x BN tiles): halves each SM's B-operand traffic
   // from L2.  GEMMs with >= 2 row blocks, BN >= 128, TMA epilogue, and >= 60
   // GFLOP: interleaved A/B timing (MP_GEMM_NO_PAIR on / off, round 1) had the pair
@@ -773,9 +781,36 @@ mp_status gemm_bf16(const mp_gemm_desc& g, cudaStream_t st, const GemmCe* ce = n
     a.m_blocks = (g.M + 2 * BM - 1) / (2 * BM);
     a.num_tiles = a.m_blocks * a.n_blocks * g.batch;
   }
+  // Raster: by default consecutive tiles share the B panel (m fastest).  When A
+  // is the large operand and B fits comfortably in L2 (e.g. the logit-layer
+  // weight gradient dE = dlogits^T Z, A = 210 MB, B = 9 MB), walk n fastest so
+  // every A panel is streamed from DRAM once instead of once per n-block.
+  // More generally: in m-fast order every wave of concurrent tiles spans all m-blocks,
+  // so A is streamed once per wave unless it stays L2-resident, while B is read once;
+  // n-fast is the transpose.  Pick the order with the smaller estimated DRAM
+  // operand traffic (an operand up to ~40 MB counts as L2-resident across waves).
+  {
+    const double a_bytes = 2.0 * g.M * (double)g.K * g.batch, b_bytes = 2.0 * g.N * (double)g.K * g.batch;
+    const double conc = a.pair ? sm_cap() / 2 : sm_cap();   // tiles in flight (pair tiles are 256 rows)
+    const double waves = std::max(1.0, std::ceil((double)a.num_tiles / std::max(1.0, conc)));
+    const double l2 = 40e6;
+    const double m_fast = (a_bytes > l2 ? a_bytes * std::min(waves, (double)a.n_blocks) : a_bytes) + b_bytes;
+    const double n_fast = (b_bytes > l2 ? b_bytes * std::min(waves, (double)a.m_blocks) : b_bytes) + a_bytes;
+    static const bool old_raster = getenv("MP_GEMM_RASTER_V1") != nullptr;   // A/B: round-1 rule
+    if (old_raster)
+      a.n_fast = (a.n_blocks > 1 && a_bytes > 2.0 * b_bytes && b_bytes < 32e6) ? 1 : 0;
+    else
+      a.n_fast = (a.n_blocks > 1 && n_fast < 0.95 * m_fast) ? 1 : 0;
+  }
   a.stream_k = 0;
+  a.sk_first = 0;
   static const bool no_sk = getenv("MP_GEMM_NO_STREAMK") != nullptr;
   a.stream_k = want_stream_k(a) && !no_sk;
+  if (a.stream_k) {   // whole tiles for the full waves, stream-K only for the partial last wave
+    static const bool sk_all = getenv("MP_GEMM_STREAMK_ALL") != nullptr;   // A/B: round-1 pure stream-K
+    const int G = a.pair ? sm_cap() / 2 : sm_cap();
+    a.sk_first = sk_all ? 0 : (a.num_tiles / G) * G;
+  }
   CUtensorMap ta, tb;
   bool ok = g.a_major ? make_map(&ta, g.A, g.M, g.K, g.batch, g.lda, g.strideA, BK)
                       : make_map(&ta, g.A, g.K, g.M, g.batch, g.lda, g.strideA, BM);
@@ -807,7 +842,7 @@ mp_status gemm_fp32(const mp_gemm_desc& g, cudaStream_t st) {
   if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.batch <= 0) return set_err(MP_EINVAL, "gemm: empty shape");
   if (g.act) return set_err(MP_EUNSUPPORTED, "gemm: the fused GeLU epilogue is bf16-only");
   dim3 grid((g.M + SB_M - 1) / SB_M, (g.N + SB_N - 1) / SB_N, g.batch);
-  simt_gemm_kernel<<<grid, 256, 0, st>>>(g, grid.x, grid.y);
+  pdl_launch(simt_gemm_kernel, grid, 256, 0, st, g, (int)grid.x, (int)grid.y);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_err(MP_ECUDA, "simt gemm launch: %s", cudaGetErrorString(e));
   return MP_OK;

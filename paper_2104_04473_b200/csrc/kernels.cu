@@ -5,6 +5,7 @@
 // warp per row), reduces with warp shuffles, and computes in fp32.
 #include "kernels.cuh"
 #include "common.h"
+#include "launch.cuh"
 #include "dropout.cuh"
 
 #include <algorithm>
@@ -198,6 +199,7 @@ __global__ void __launch_bounds__(ROW_THREADS) ln_fwd_kernel(const T* __restrict
                                                       T* __restrict__ out, float* __restrict__ mean,
                                                       float* __restrict__ rstd, int h, float eps, Dropout dp, int R,
                                                       int RG, int NG) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float2 red[2][ROW_MAX_NG][ROW_MAX_WARPS];
   const int grp = threadIdx.x / RG, lt = threadIdx.x - grp * RG;
@@ -266,7 +268,7 @@ static mp_status launch_ln_fwd(const T* in, const T* bias, const T* res, T* x1, 
     const int threads = rc.RG * rc.NG;
     const long long need = (R + rc.NG - 1) / rc.NG;
     const int grid = (int)std::min<long long>(need, (long long)num_sms() * resident_ctas(kern, threads, 0));
-    kern<<<grid, threads, 0, st>>>(in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R, rc.RG, rc.NG);
+    pdl_launch(kern, grid, threads, 0, st, in, bias, res, x1, g, b, out, mean, rstd, h, eps, dp, R, rc.RG, rc.NG);
   };
   switch (rc.NV) {
     case 1: go(ln_fwd_kernel<T, 1, MODE, RED>); break;
@@ -297,6 +299,7 @@ template <class T, bool RED = false>
 __global__ void bias_add_residual_kernel(const T* __restrict__ yv, const T* __restrict__ bias,
                                          const T* __restrict__ r, T* __restrict__ out, long long nvec, int hv,
                                          Dropout dp) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
     float a[V], bb[V], rr[V];
@@ -329,9 +332,9 @@ mp_status bias_add_residual(const T* yv, const T* bias, const T* r, T* out, long
   if (h % V) return set_err(MP_EINVAL, "bias_add_residual: h %% %d", V);
   long long nvec = R * h / V;
   if (red)
-    bias_add_residual_kernel<T, true><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V, dp);
+    pdl_launch(bias_add_residual_kernel<T, true>, ew_grid(nvec), 256, 0, st, yv, bias, r, out, nvec, h / V, dp);
   else
-    bias_add_residual_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, bias, r, out, nvec, h / V, dp);
+    pdl_launch(bias_add_residual_kernel<T>, ew_grid(nvec), 256, 0, st, yv, bias, r, out, nvec, h / V, dp);
   LAUNCH_CHECK();
 }
 
@@ -362,6 +365,7 @@ __global__ void __launch_bounds__(256) ln_bwd_dx_kernel(const T* __restrict__ dy
                                                         const T* __restrict__ g, const float* __restrict__ mean,
                                                         const float* __restrict__ rstd, const T* __restrict__ dres,
                                                         T* __restrict__ dx, int h, T* __restrict__ dy_copy, int R) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float2 red[32];
   const int nvec = h / V;
@@ -439,6 +443,7 @@ static inline dim3 ct_grid(int nv, int R) { return dim3((nv + CT_X - 1) / CT_X, 
 template <class T>
 __global__ void __launch_bounds__(CT_X * CT_Y) colsum_kernel(const T* __restrict__ X, float* __restrict__ out, int R,
                                                             int N) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float red[CT_Y * CT_X * V];
   const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
@@ -461,7 +466,7 @@ template <class T>
 mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "colsum: N %% %d", V);
-  colsum_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(X, out, R, N);
+  pdl_launch(colsum_kernel<T>, ct_grid(N / V, R), CT_X * CT_Y, 0, st, X, out, R, N);
   LAUNCH_CHECK();
 }
 
@@ -469,6 +474,7 @@ mp_status colsum_accum(const T* X, float* out, int R, int N, cudaStream_t st) {
 template <class T>
 __global__ void __launch_bounds__(CT_X * CT_Y) dropout_colsum_kernel(const T* __restrict__ dY, T* __restrict__ dZ,
                                                                     float* __restrict__ out, int R, int N, Dropout dp) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float red[CT_Y * CT_X * V];
   const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
@@ -496,7 +502,7 @@ template <class T>
 mp_status dropout_colsum(const T* dY, T* dZ, float* out, int R, int N, Dropout dp, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "dropout_colsum: N %% %d", V);
-  dropout_colsum_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(dY, dZ, out, R, N, dp);
+  pdl_launch(dropout_colsum_kernel<T>, ct_grid(N / V, R), CT_X * CT_Y, 0, st, dY, dZ, out, R, N, dp);
   LAUNCH_CHECK();
 }
 
@@ -510,6 +516,7 @@ __global__ void __launch_bounds__(CT_X * CT_Y) ln_bwd_gb_kernel(const T* __restr
                                                                float* __restrict__ dgamma, float* __restrict__ dbeta,
                                                                float* __restrict__ dres_sum, float* __restrict__ dx_sum,
                                                                int R, int h) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float red[CT_Y * CT_X * V];
   const int tx = threadIdx.x % CT_X, ty = threadIdx.x / CT_X;
@@ -557,18 +564,18 @@ mp_status layernorm_bwd(const T* dy, const T* x, const T* g, const float* mean, 
   const int nv = h / VW<T>::N;
   if (nv > LNB_MAXV * 256) return set_err(MP_EINVAL, "layernorm_bwd: h=%d too large", h);
   if (dy_copy) {
-    ln_bwd_dx_kernel<T, true><<<row_grid(R, nv), row_threads(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h,
+    pdl_launch(ln_bwd_dx_kernel<T, true>, row_grid(R, nv), row_threads(nv), 0, st, dy, x, g, mean, rstd, dres, dx, h,
                                                                             dy_copy, R);
     dy = dy_copy;
   } else {
-    ln_bwd_dx_kernel<T><<<row_grid(R, nv), row_threads(nv), 0, st>>>(dy, x, g, mean, rstd, dres, dx, h, nullptr, R);
+    pdl_launch(ln_bwd_dx_kernel<T>, row_grid(R, nv), row_threads(nv), 0, st, dy, x, g, mean, rstd, dres, dx, h, nullptr, R);
   }
   count_launch();
   if (dres_sum || dx_sum)
-    ln_bwd_gb_kernel<T, true><<<ct_grid(nv, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, dres, dx, dgamma, dbeta,
+    pdl_launch(ln_bwd_gb_kernel<T, true>, ct_grid(nv, R), CT_X * CT_Y, 0, st, dy, x, mean, rstd, dres, dx, dgamma, dbeta,
                                                                       dres_sum, dx_sum, R, h);
   else
-    ln_bwd_gb_kernel<T, false><<<ct_grid(nv, R), CT_X * CT_Y, 0, st>>>(dy, x, mean, rstd, nullptr, nullptr, dgamma,
+    pdl_launch(ln_bwd_gb_kernel<T, false>, ct_grid(nv, R), CT_X * CT_Y, 0, st, dy, x, mean, rstd, nullptr, nullptr, dgamma,
                                                                        dbeta, nullptr, nullptr, R, h);
   LAUNCH_CHECK();
 }
@@ -584,6 +591,7 @@ __device__ __forceinline__ float gelu_f(float u, float* dgelu) {
 template <class T>
 __global__ void bias_gelu_fwd_kernel(const T* __restrict__ yv, const T* __restrict__ b, T* __restrict__ out,
                                      long long nvec, int nv_row) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nvec; i += (long long)gridDim.x * blockDim.x) {
     float a[V], bb[V];
@@ -600,7 +608,7 @@ mp_status bias_gelu_fwd(const T* yv, const T* b, T* out, long long R, int N, cud
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "bias_gelu: N %% %d", V);
   long long nvec = R * N / V;
-  bias_gelu_fwd_kernel<T><<<ew_grid(nvec), 256, 0, st>>>(yv, b, out, nvec, N / V);
+  pdl_launch(bias_gelu_fwd_kernel<T>, ew_grid(nvec), 256, 0, st, yv, b, out, nvec, N / V);
   LAUNCH_CHECK();
 }
 
@@ -608,6 +616,7 @@ template <class T>
 __global__ void __launch_bounds__(CT_X * CT_Y) bias_gelu_bwd_kernel(const T* dh, const T* __restrict__ yv,
                                                                    const T* __restrict__ b, T* du,
                                                                    float* __restrict__ db, int R, int N) {
+  pdl_entry();
   // du may alias dh (each element is read, then written, by the same thread)
   constexpr int V = VW<T>::N;
   __shared__ float red[CT_Y * CT_X * V];
@@ -644,7 +653,7 @@ template <class T>
 mp_status bias_gelu_bwd(const T* dh, const T* yv, const T* b, T* du, float* db, int R, int N, cudaStream_t st) {
   constexpr int V = VW<T>::N;
   if (N % V) return set_err(MP_EINVAL, "bias_gelu_bwd: N %% %d", V);
-  bias_gelu_bwd_kernel<T><<<ct_grid(N / V, R), CT_X * CT_Y, 0, st>>>(dh, yv, b, du, db, R, N);
+  pdl_launch(bias_gelu_bwd_kernel<T>, ct_grid(N / V, R), CT_X * CT_Y, 0, st, dh, yv, b, du, db, R, N);
   LAUNCH_CHECK();
 }
 
@@ -674,6 +683,7 @@ __device__ __forceinline__ float block_sum128(float a, float* red) {
 
 template <class T, int VPT>
 __global__ void __launch_bounds__(SM_THREADS) softmax_fwd_kernel(T* __restrict__ S, int s, float scale_log2) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float red[4];
   const long long rg = blockIdx.x;
@@ -723,6 +733,7 @@ __global__ void __launch_bounds__(SM_THREADS) softmax_fwd_kernel(T* __restrict__
 template <class T, int VPT>
 __global__ void __launch_bounds__(SM_THREADS) softmax_bwd_kernel(T* __restrict__ dP, const T* __restrict__ P, int s,
                                                                  float scale, Dropout dp) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   __shared__ float red[4];
   const long long rg = blockIdx.x;
@@ -783,9 +794,9 @@ mp_status softmax_causal_fwd(T* S, long long z, int s, float scale, cudaStream_t
   const long long rows = z * s;
   if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "softmax: too many rows");
   const float sl2 = scale * 1.4426950408889634f;
-  if (vpt == 1) softmax_fwd_kernel<T, 1><<<(unsigned)rows, SM_THREADS, 0, st>>>(S, s, sl2);
-  else if (vpt == 2) softmax_fwd_kernel<T, 2><<<(unsigned)rows, SM_THREADS, 0, st>>>(S, s, sl2);
-  else softmax_fwd_kernel<T, 4><<<(unsigned)rows, SM_THREADS, 0, st>>>(S, s, sl2);
+  if (vpt == 1) pdl_launch(softmax_fwd_kernel<T, 1>, (unsigned)rows, SM_THREADS, 0, st, S, s, sl2);
+  else if (vpt == 2) pdl_launch(softmax_fwd_kernel<T, 2>, (unsigned)rows, SM_THREADS, 0, st, S, s, sl2);
+  else pdl_launch(softmax_fwd_kernel<T, 4>, (unsigned)rows, SM_THREADS, 0, st, S, s, sl2);
   LAUNCH_CHECK();
 }
 
@@ -797,9 +808,9 @@ mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale,
   if (vpt < 0) return set_err(MP_EINVAL, "softmax: s=%d too long", s);
   const long long rows = z * s;
   if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "softmax: too many rows");
-  if (vpt == 1) softmax_bwd_kernel<T, 1><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale, dp);
-  else if (vpt == 2) softmax_bwd_kernel<T, 2><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale, dp);
-  else softmax_bwd_kernel<T, 4><<<(unsigned)rows, SM_THREADS, 0, st>>>(dP, P, s, scale, dp);
+  if (vpt == 1) pdl_launch(softmax_bwd_kernel<T, 1>, (unsigned)rows, SM_THREADS, 0, st, dP, P, s, scale, dp);
+  else if (vpt == 2) pdl_launch(softmax_bwd_kernel<T, 2>, (unsigned)rows, SM_THREADS, 0, st, dP, P, s, scale, dp);
+  else pdl_launch(softmax_bwd_kernel<T, 4>, (unsigned)rows, SM_THREADS, 0, st, dP, P, s, scale, dp);
   LAUNCH_CHECK();
 }
 
@@ -808,6 +819,7 @@ mp_status softmax_causal_bwd(T* dP, const T* P, long long z, int s, float scale,
 template <class T>
 __global__ void __launch_bounds__(SM_THREADS) attn_dropout_kernel(const T* __restrict__ P, T* __restrict__ Pd, int s,
                                                                   Dropout dp) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   const long long rg = blockIdx.x;
   const int i = (int)(rg % s);
@@ -827,7 +839,7 @@ template <class T>
 mp_status attn_dropout(const T* P, T* Pd, long long z, int s, Dropout dp, cudaStream_t st) {
   const long long rows = z * s;
   if (rows > 0x7fffffffLL) return set_err(MP_EINVAL, "attn_dropout: too many rows");
-  attn_dropout_kernel<T><<<(unsigned)rows, SM_THREADS, 0, st>>>(P, Pd, s, dp);
+  pdl_launch(attn_dropout_kernel<T>, (unsigned)rows, SM_THREADS, 0, st, P, Pd, s, dp);
   LAUNCH_CHECK();
 }
 
@@ -835,6 +847,7 @@ mp_status attn_dropout(const T* P, T* Pd, long long z, int s, Dropout dp, cudaSt
 template <class T>
 __global__ void embed_fwd_kernel(const int* __restrict__ tok, int tok_ld, const T* __restrict__ E, int v0, int Vr,
                                  const T* __restrict__ pos, T* __restrict__ X, int b, int h) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   const int row = blockIdx.x;           // row = i*b + beta
   const int i = row / b, beta = row % b;
@@ -857,7 +870,7 @@ template <class T>
 mp_status embed_fwd(const int* tok, int tok_ld, const T* E, int v0, int Vr, const T* pos, T* X, int s, int b, int h,
                     cudaStream_t st) {
   if (h % VW<T>::N) return set_err(MP_EINVAL, "embed: h");
-  embed_fwd_kernel<T><<<s * b, std::min(256, std::max(32, h / VW<T>::N)), 0, st>>>(tok, tok_ld, E, v0, Vr, pos, X, b,
+  pdl_launch(embed_fwd_kernel<T>, s * b, std::min(256, std::max(32, h / VW<T>::N)), 0, st, tok, tok_ld, E, v0, Vr, pos, X, b,
                                                                                     h);
   LAUNCH_CHECK();
 }
@@ -865,6 +878,7 @@ mp_status embed_fwd(const int* tok, int tok_ld, const T* E, int v0, int Vr, cons
 template <class T>
 __global__ void embed_bwd_kernel(const int* __restrict__ tok, int tok_ld, const T* __restrict__ dX, int v0, int Vr,
                                  float* __restrict__ dE, float* __restrict__ dpos, int b, int h) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   const int row = blockIdx.x;
   const int i = row / b, beta = row % b;
@@ -885,13 +899,14 @@ template <class T>
 mp_status embed_bwd(const int* tok, int tok_ld, const T* dX, int v0, int Vr, float* dE, float* dpos, int s, int b,
                     int h, cudaStream_t st) {
   if (h % VW<T>::N) return set_err(MP_EINVAL, "embed: h");
-  embed_bwd_kernel<T><<<s * b, std::min(256, std::max(32, h / VW<T>::N)), 0, st>>>(tok, tok_ld, dX, v0, Vr, dE, dpos,
+  pdl_launch(embed_bwd_kernel<T>, s * b, std::min(256, std::max(32, h / VW<T>::N)), 0, st, tok, tok_ld, dX, v0, Vr, dE, dpos,
                                                                                     b, h);
   LAUNCH_CHECK();
 }
 
 // ---------------------------------------------------------- cross-entropy
 __global__ void ce_rowmax_kernel(const float* __restrict__ L, float* __restrict__ rowmax, int Vr) {
+  pdl_entry();
   __shared__ float red[32];
   const float* p = L + (long long)blockIdx.x * Vr;
   float m = -FLT_MAX;
@@ -905,7 +920,7 @@ __global__ void ce_rowmax_kernel(const float* __restrict__ L, float* __restrict_
 
 mp_status ce_rowmax(const float* logits, float* rowmax, int R, int Vr, cudaStream_t st) {
   if (Vr % 4) return set_err(MP_EINVAL, "ce: Vr %% 4");
-  ce_rowmax_kernel<<<R, 256, 0, st>>>(logits, rowmax, Vr);
+  pdl_launch(ce_rowmax_kernel, R, 256, 0, st, logits, rowmax, Vr);
   LAUNCH_CHECK();
 }
 
@@ -916,6 +931,7 @@ __device__ __forceinline__ int ce_label(const int* lab, int lab_ld, int row, int
 __global__ void ce_sum_kernel(const float* __restrict__ L, const float* __restrict__ rowmax,
                               const int* __restrict__ lab, int lab_ld, int b, int v0, float* __restrict__ out, int R,
                               int Vr) {
+  pdl_entry();
   __shared__ float2 red[32];
   const int row = blockIdx.x;
   const float* p = L + (long long)row * Vr;
@@ -935,7 +951,7 @@ __global__ void ce_sum_kernel(const float* __restrict__ L, const float* __restri
 
 mp_status ce_sumexp_target(const float* logits, const float* rowmax, const int* lab, int lab_ld, int s, int b, int v0,
                            float* sum_tgt, int R, int Vr, cudaStream_t st) {
-  ce_sum_kernel<<<R, 256, 0, st>>>(logits, rowmax, lab, lab_ld, b, v0, sum_tgt, R, Vr);
+  pdl_launch(ce_sum_kernel, R, 256, 0, st, logits, rowmax, lab, lab_ld, b, v0, sum_tgt, R, Vr);
   LAUNCH_CHECK();
 }
 
@@ -943,6 +959,7 @@ template <class T>
 __global__ void ce_grad_kernel(const float* __restrict__ L, const float* __restrict__ rowmax,
                                const float* __restrict__ st, const int* __restrict__ lab, int lab_ld, int b, int v0,
                                float scale, T* __restrict__ dL, float* __restrict__ loss_acc, int R, int Vr) {
+  pdl_entry();
   constexpr int V = VW<T>::N;
   const int row = blockIdx.x;
   const float* p = L + (long long)row * Vr;
@@ -962,7 +979,7 @@ template <class T>
 mp_status ce_loss_grad(const float* logits, const float* rowmax, const float* sum_tgt, const int* lab, int lab_ld,
                        int s, int b, int v0, float scale, T* dlogits, float* loss_acc, int R, int Vr, cudaStream_t st) {
   if (Vr % VW<T>::N) return set_err(MP_EINVAL, "ce: Vr");
-  ce_grad_kernel<T><<<R, 256, 0, st>>>(logits, rowmax, sum_tgt, lab, lab_ld, b, v0, scale, dlogits, loss_acc, R, Vr);
+  pdl_launch(ce_grad_kernel<T>, R, 256, 0, st, logits, rowmax, sum_tgt, lab, lab_ld, b, v0, scale, dlogits, loss_acc, R, Vr);
   LAUNCH_CHECK();
 }
 
@@ -976,6 +993,7 @@ __global__ void ce_stats_kernel(const float2* __restrict__ part, int np, const f
                                 const int* __restrict__ lab, int lab_ld, int b, int v0, int Vr,
                                 float* __restrict__ mx, float* __restrict__ mx_local, float* __restrict__ stt,
                                 int R) {
+  pdl_entry();
   const int lane = threadIdx.x % 32;
   const int row = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
   if (row >= R) return;
@@ -1001,17 +1019,18 @@ __global__ void ce_stats_kernel(const float2* __restrict__ part, int np, const f
 // after the TP max-reduction of mx: sum-exp relative to the global row max
 __global__ void ce_rescale_kernel(const float* __restrict__ mx, const float* __restrict__ mx_local,
                                   float* __restrict__ stt, int R) {
+  pdl_entry();
   const int r = blockIdx.x * blockDim.x + threadIdx.x;
   if (r < R) stt[r] *= exp2f((mx_local[r] - mx[r]) * 1.4426950408889634f);
 }
 
 mp_status ce_stats(const float2* part, int np, const float* tgt, const int* lab, int lab_ld, int b, int v0, int Vr,
                    float* mx, float* mx_local, float* stt, int R, cudaStream_t st) {
-  ce_stats_kernel<<<(R + 7) / 8, 256, 0, st>>>(part, np, tgt, lab, lab_ld, b, v0, Vr, mx, mx_local, stt, R);
+  pdl_launch(ce_stats_kernel, (R + 7) / 8, 256, 0, st, part, np, tgt, lab, lab_ld, b, v0, Vr, mx, mx_local, stt, R);
   LAUNCH_CHECK();
 }
 mp_status ce_rescale(const float* mx, const float* mx_local, float* stt, int R, cudaStream_t st) {
-  ce_rescale_kernel<<<(R + 255) / 256, 256, 0, st>>>(mx, mx_local, stt, R);
+  pdl_launch(ce_rescale_kernel, (R + 255) / 256, 256, 0, st, mx, mx_local, stt, R);
   LAUNCH_CHECK();
 }
 
@@ -1022,6 +1041,7 @@ __global__ void __launch_bounds__(256) ce_grad_inplace_kernel(__nv_bfloat16* __r
                                                               const float* __restrict__ st, const int* __restrict__ lab,
                                                               int lab_ld, int b, int v0, float scale,
                                                               float* __restrict__ loss_acc, int R, int Vr) {
+  pdl_entry();
   const int row = blockIdx.x;
   __nv_bfloat16* p = L + (long long)row * Vr;
   const float mxl2 = rowmax[row] * 1.4426950408889634f, sum = st[row];
@@ -1040,7 +1060,7 @@ __global__ void __launch_bounds__(256) ce_grad_inplace_kernel(__nv_bfloat16* __r
 mp_status ce_grad_inplace(__nv_bfloat16* logits, const float* rowmax, const float* sum_tgt, const int* lab, int lab_ld,
                           int b, int v0, float scale, float* loss_acc, int R, int Vr, cudaStream_t st) {
   if (Vr % 8) return set_err(MP_EINVAL, "ce: Vr %% 8");
-  ce_grad_inplace_kernel<<<R, 256, 0, st>>>(logits, rowmax, sum_tgt, lab, lab_ld, b, v0, scale, loss_acc, R, Vr);
+  pdl_launch(ce_grad_inplace_kernel, R, 256, 0, st, logits, rowmax, sum_tgt, lab, lab_ld, b, v0, scale, loss_acc, R, Vr);
   LAUNCH_CHECK();
 }
 
@@ -1060,6 +1080,7 @@ template <class T>
 __global__ void adam_kernel(float* w, const float* __restrict__ g, float* __restrict__ m1,
                             float* __restrict__ m2, T* ws /* may alias w (fp32) */, long long n, float lr, float b1, float b2,
                             float eps, float bc1, float bc2) {
+  pdl_entry();
   const long long n4 = n / 4;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     float4 wv = reinterpret_cast<float4*>(w)[i];
@@ -1094,12 +1115,13 @@ mp_status adam_step(float* w, const float* g, float* m1, float* m2, T* w_store, 
   auto al = [](const void* p, int a) { return (reinterpret_cast<uintptr_t>(p) & (a - 1)) == 0; };
   if (!al(w, 16) || !al(g, 16) || !al(m1, 16) || !al(m2, 16) || !al(w_store, sizeof(T) * 4))
     return set_err(MP_EINVAL, "adam_step: arrays must be 16-byte aligned");
-  adam_kernel<T><<<ew_grid(n / 4 + 1), 256, 0, st>>>(w, g, m1, m2, w_store, n, lr, b1, b2, eps, bc1, bc2);
+  pdl_launch(adam_kernel<T>, ew_grid(n / 4 + 1), 256, 0, st, w, g, m1, m2, w_store, n, lr, b1, b2, eps, bc1, bc2);
   LAUNCH_CHECK();
 }
 
 template <class T>
 __global__ void cast_kernel(const float* __restrict__ s, T* __restrict__ d, long long n) {
+  pdl_entry();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     if constexpr (sizeof(T) == 2) d[i] = __float2bfloat16_rn(s[i]); else d[i] = s[i];
   }
@@ -1107,7 +1129,7 @@ __global__ void cast_kernel(const float* __restrict__ s, T* __restrict__ d, long
 
 template <class T>
 mp_status cast_from_f32(const float* src, T* dst, long long n, cudaStream_t st) {
-  cast_kernel<T><<<ew_grid(n), 256, 0, st>>>(src, dst, n);
+  pdl_launch(cast_kernel<T>, ew_grid(n), 256, 0, st, src, dst, n);
   LAUNCH_CHECK();
 }
 

@@ -1,11 +1,14 @@
-"""Per-iteration timeline of the flash backward kernel (CTA 0 = kv tile 0, all
-16 query tiles at s = 2048) from the in-kernel %globaltimer stamps (MP_FA_TRACE).
+"""Per-iteration timeline of the flash kernels from the in-kernel %globaltimer
+stamps of CTA 0 (MP_FA_TRACE), 1.7B b=2 shape.
 
-    MP_FA_TRACE=1 python tools/fa_trace.py
+    MP_FA_TRACE=1 python tools/fa_trace.py [--fwd]
 
-Events per iteration: 0 loads issued (producer), 1 S/dP products issued (MMA),
-2 dV/dK/dQ products issued (MMA), 3 S/dP ready (compute), 4 P/dS written,
-5 dQ ready, 6 dQ staged.  Printed relative to the first event, in ns.
+Backward (CTA 0 = kv tile 0, all 16 query tiles): 0 loads issued (producer),
+1 S/dP products issued (MMA), 2 dV/dK/dQ products issued, 3 S/dP ready
+(compute), 4 P/dS written, 5 dQ ready, 6 dQ staged.
+Forward (CTA 0 = the last query tile, 16 kv tiles): 0 K issued, 1 V issued,
+2 S product issued, 3 P.V issued, 4 S read, 5 max / rescale done, 6 P written.
+Printed relative to the first event, in ns.
 """
 import ctypes
 import json
@@ -29,7 +32,11 @@ def main():
     dq = torch.zeros_like(q)
     ws = torch.zeros(mp.raw("mp_op_flash_attn_bwd_ws_floats", s, b, heads, hd), device="cuda")
     mp.call("mp_op_flash_attn_fwd", q.data_ptr(), ctx.data_ptr(), lse.data_ptr(), s, b, heads, hd, None)
+    fwd = "--fwd" in sys.argv
     for _ in range(3):
+        if fwd:
+            mp.call("mp_op_flash_attn_fwd", q.data_ptr(), ctx.data_ptr(), lse.data_ptr(), s, b, heads, hd, None)
+            continue
         mp.call("mp_op_flash_attn_bwd", q.data_ptr(), ctx.data_ptr(), dc.data_ptr(), lse.data_ptr(), dq.data_ptr(),
                 ws.data_ptr(), s, b, heads, hd, None)
     torch.cuda.synchronize()
