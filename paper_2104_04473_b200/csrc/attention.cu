@@ -225,15 +225,21 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       tc_fence_before();
       mbar_arrive(&s_empty[sb]);
       if (threadIdx.x == 64) FA_TRACE(4, j);
-      float mx = -FLT_MAX;
+      // row max over 8 independent chains (a single 128-long fmax chain is latency-bound:
+      // ncu r02 "stalled_wait" dominated the softmax warps)
+      float mxa[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mxa[k] = -FLT_MAX;
       if (diag) {
 #pragma unroll
         for (int e = 0; e < 128; ++e)
-          if (e <= r) mx = fmaxf(mx, __uint_as_float(sv[e]));
+          if (e <= r) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(sv[e]));
       } else {
 #pragma unroll
-        for (int e = 0; e < 128; ++e) mx = fmaxf(mx, __uint_as_float(sv[e]));
+        for (int e = 0; e < 128; ++e) mxa[e & 7] = fmaxf(mxa[e & 7], __uint_as_float(sv[e]));
       }
+      const float mx = fmaxf(fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3])),
+                             fmaxf(fmaxf(mxa[4], mxa[5]), fmaxf(mxa[6], mxa[7])));
       const float mt = mx * g.scale_log2;
       // raise the reference max only when this tile exceeds it by more than 2^RESCALE_LOG2
       const bool need = __any_sync(0xffffffffu, mt > m + RESCALE_LOG2);
@@ -262,9 +268,10 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
       const uint32_t prow = smem_u32(sP + sb * P_BYTES) + r * 128;
       // P = exp2(s * scale_log2 - m) -> bf16 into the swizzled P tile (dropped
       // entries zeroed and kept ones scaled; the row sum uses the undropped values)
-      float rs = 0.f;
+      float rsa[4] = {0.f, 0.f, 0.f, 0.f};   // row sum over 4 independent chains
       constexpr bool drop = DROP;
       const int zb = z / g.dp.heads, zj = z % g.dp.heads;
+      const int cut = diag ? r : 127;          // columns > cut are masked (causal diagonal tile)
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t km = 0xffffffffu;
@@ -281,11 +288,9 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
           const int col = 32 * c + e;
           float p0 = ex2f(fmaf(__uint_as_float(sv[col]), g.scale_log2, -m));
           float p1 = ex2f(fmaf(__uint_as_float(sv[col + 1]), g.scale_log2, -m));
-          if (diag) {
-            if (col > r) p0 = 0.f;
-            if (col + 1 > r) p1 = 0.f;
-          }
-          rs += p0 + p1;
+          if (col > cut) p0 = 0.f;
+          if (col + 1 > cut) p1 = 0.f;
+          rsa[(e >> 1) & 3] += p0 + p1;
           if (drop) {
             p0 = (km >> e) & 1 ? p0 * g.dp.scale : 0.f;
             p1 = (km >> (e + 1)) & 1 ? p1 * g.dp.scale : 0.f;
@@ -302,7 +307,7 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         }
       }
       tc_fence_before();
-      l = l * alpha + rs;
+      l = l * alpha + ((rsa[0] + rsa[1]) + (rsa[2] + rsa[3]));
       fence_proxy_async_smem();        // P written by the generic proxy, read by tcgen05.mma
       mbar_arrive(p_full);
       if (threadIdx.x == 64) FA_TRACE(6, j);

@@ -8,8 +8,10 @@ SET:
   balanced  GPT-1.7B width (h=2304, l=24) with V=512 (negligible head, so the
             stages are balanced as (p-1)/(v m) assumes), t=1,
             p in {2, 4}, v in {1, 2, 3}, m in {8, 16}, b=1.
+  balanced_b2  the same layouts at b=2 (twice the work per task).
   w391      39.1B width (h=8192, a=64), l=24, t=2 x p=2, m=16, b=1,
             v in {1, 2, 3, 6}, full V=51200 head (BASELINE configs[4] sweep).
+  w391v6    only the v=6 point of w391.
 Each run is wrapped in `timeout`; a failed run records its exit code.
 """
 import json
@@ -26,8 +28,13 @@ def runs(which):
             for v in (1, 2, 3):
                 for m in (8, 16):
                     yield dict(model="1.7B", t=1, p=p, v=v, m=m, b=1, vocab=512, layers=24)
-    elif which == "w391":
-        for v in (1, 2, 3, 6):
+    elif which == "balanced_b2":
+        for p in (2, 4):
+            for v in (1, 2, 3):
+                for m in (8, 16):
+                    yield dict(model="1.7B", t=1, p=p, v=v, m=m, b=2, vocab=512, layers=24)
+    elif which in ("w391", "w391v6"):
+        for v in ((1, 2, 3, 6) if which == "w391" else (6,)):
             yield dict(model="39.1B", t=2, p=2, v=v, m=16, b=1, vocab=0, layers=24)
     else:
         raise SystemExit(f"unknown set {which}")
