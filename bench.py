@@ -510,6 +510,21 @@ def main():
     }
     if world > 1:
         out["comm"] = comm_calibration(cfg, b, t, p, d, world, m, t_step)
+        if out["comm"] is not None and ctx.tp_comm_mode() == "nvls":
+            # the default path: the same payload through the library's fused NVLS reduction
+            sec = ctx.tp_reduce_probe(b, 20)
+            from paper_2104_04473_b200 import launch
+            sec = launch.max_over_ranks(sec, world, "cuda")
+            payload = 2.0 * cfg.s * b * cfg.h
+            busbw = payload / sec / 1e9 * 2.0 * (t - 1) / t
+            out["comm"]["nvls"] = {
+                "us_per_reduction": sec * 1e6, "busbw_gbs": busbw, "nvlink_peak_gbs": 900.0, "frac": busbw / 900.0,
+                "shot": "two" if t >= 4 else "one",
+                "share_of_step_upper_bound": 4 * cfg.l * m * sec / t_step,
+                "how": "mp_tp_reduce_probe: next symmetric buffer, NVLS barrier (one-shot) or slab reduce-load + "
+                       "multicast store + barrier (two-shot), then the consuming bias-residual kernel reading the "
+                       "t-way sum of s*b*h bf16; CUDA events, 20 reps after 3, max over ranks; busbw convention "
+                       "of NCCL (payload * 2(t-1)/t / time) vs 900 GB/s NVLink 5 per direction"}
     if e2e:
         out["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

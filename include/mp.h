@@ -221,6 +221,15 @@ mp_status mp_run_batch(mp_ctx* ctx, int B, int b, int m, mp_schedule sched, cons
  * callers can bracket batches with CUDA events on it. */
 void* mp_compute_stream(mp_ctx* ctx);
 
+/* NVLink calibration of the fused g / f reduction exactly as the layer
+ * runs it on the NVLS path: per repetition the next symmetric buffer, the NVLS barrier
+ * (one-shot) or slab reduce-load + multicast store + barrier (two-shot, t >= 4), and
+ * the consuming bias-residual kernel that reads the t-way sum of s*b*h elements.
+ * Collective over the TP group (every TP rank calls it with the same b, iters).
+ * *seconds = time per reduction, CUDA events on the compute stream after 3 warm-up
+ * repetitions.  MP_EUNSUPPORTED when t = 1 or the context runs the NCCL path. */
+mp_status mp_tp_reduce_probe(mp_ctx* ctx, int b, int iters, double* seconds);
+
 /* Transport the layer's g / f all-reduces use on this rank: MP_TP_COMM_NCCL or
  * MP_TP_COMM_NVLS (decided collectively at the first layer call with t > 1;
  * MP_TP_COMM_AUTO before that; MP_TP_COMM_NCCL when t = 1, no collective). */

@@ -875,6 +875,11 @@ mp_status embed_fwd(const int* tok, int tok_ld, const T* E, int v0, int Vr, cons
   LAUNCH_CHECK();
 }
 
+__device__ __forceinline__ void red_v4(float* p, const float* v) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3])
+               : "memory");
+}
+
 template <class T>
 __global__ void embed_bwd_kernel(const int* __restrict__ tok, int tok_ld, const T* __restrict__ dX, int v0, int Vr,
                                  float* __restrict__ dE, float* __restrict__ dpos, int b, int h) {
@@ -887,10 +892,11 @@ __global__ void embed_bwd_kernel(const int* __restrict__ tok, int tok_ld, const 
   for (int vi = threadIdx.x; vi < h / V; vi += blockDim.x) {
     float d[V];
     ld_vec(dX + (long long)row * h + vi * V, d);
+    // vector reductions (red.global.add.v4.f32): a quarter of the atomic operations
 #pragma unroll
-    for (int e = 0; e < V; ++e) {
-      if (own) atomicAdd(dE + (long long)id * h + vi * V + e, d[e]);
-      if (dpos) atomicAdd(dpos + (long long)i * h + vi * V + e, d[e]);
+    for (int e = 0; e < V; e += 4) {
+      if (own) red_v4(dE + (long long)id * h + vi * V + e, d + e);
+      if (dpos) red_v4(dpos + (long long)i * h + vi * V + e, d + e);
     }
   }
 }

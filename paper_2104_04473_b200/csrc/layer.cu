@@ -426,6 +426,49 @@ static mp_status layer_bwd_t(mp_ctx* c, int layer, const LayerStash& st, const v
   return MP_OK;
 }
 
+// Calibration of the fused g / f reduction as the layer runs it (NVLS path): per repetition
+// next buffer -> barrier (one-shot) or slab reduce-load + multicast store + barrier
+// (two-shot) -> the consuming bias-residual kernel reading the sum.  Collective over the
+// TP group.  Returns seconds per reduction (CUDA events on the compute stream).
+template <class T>
+static mp_status tp_probe_t(mp_ctx* c, int b, int iters, double* seconds) {
+  const Dims d = dims(c, b);
+  MP_TRY(ensure_workspace(c, b));
+  if (!c->tps.on) return set_err(MP_EUNSUPPORTED, "tp probe: the NVLS path is not active on this context");
+  const size_t n = (size_t)d.T * d.h;
+  void* blk = nullptr;
+  MP_TRY(alloc_async(c, &blk, al256(n * c->esz) + al256(d.h * c->esz) + al256(n * c->esz), c->cs));
+  char* base = (char*)blk;
+  T* out = (T*)base;
+  T* zb = (T*)(base + al256(n * c->esz));
+  T* zr = (T*)(base + al256(n * c->esz) + al256(d.h * c->esz));
+  MP_CUDA(cudaMemsetAsync(zb, 0, d.h * c->esz, c->cs));
+  MP_CUDA(cudaMemsetAsync(zr, 0, n * c->esz, c->cs));
+  const bool two = tp_sym_two_shot(c);
+  auto one = [&]() -> mp_status {
+    void* w; const void* r;
+    tp_sym_next(c, &w, &r);
+    if (two) MP_TRY(tp_sym_reduce_two_shot(c, n, c->cs, &r));
+    else MP_TRY(tp_sym_barrier(c, c->cs));
+    return bias_add_residual<T>((const T*)r, zb, zr, out, d.T, d.h, c->cs, Dropout{}, !two);
+  };
+  for (int i = 0; i < 3; ++i) MP_TRY(one());
+  cudaEvent_t e0 = c->events.at(0), e1 = c->events.at(1);
+  MP_CUDA(cudaEventRecord(e0, c->cs));
+  for (int i = 0; i < iters; ++i) MP_TRY(one());
+  MP_CUDA(cudaEventRecord(e1, c->cs));
+  MP_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  MP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *seconds = ms * 1e-3 / iters;
+  MP_CUDA(cudaFreeAsync(blk, c->cs));
+  return MP_OK;
+}
+mp_status tp_reduce_probe(mp_ctx* c, int b, int iters, double* seconds) {
+  return c->cfg.dtype == MP_BF16 ? tp_probe_t<__nv_bfloat16>(c, b, iters, seconds)
+                                 : tp_probe_t<float>(c, b, iters, seconds);
+}
+
 mp_status layer_fwd(mp_ctx* c, int layer, int b, const void* x, void* y, LayerStash& st) {
   return c->cfg.dtype == MP_BF16 ? layer_fwd_t<__nv_bfloat16>(c, layer, b, x, y, st)
                                  : layer_fwd_t<float>(c, layer, b, x, y, st);

@@ -16,6 +16,8 @@ mp_status embed_backward(mp_ctx* c, const int* dtok, int tok_ld, int b, const vo
 // c->head_dl / c->head_z and the dE GEMM is left to head_dE_deferred at the flush.
 mp_status head_fwd_bwd(mp_ctx* c, const void* X, const int* dlab, int lab_ld, int b, float scale, void* dX,
                        int defer_slot = -1);
+// seconds per fused g / f reduction of s*b*h elements on the NVLS path (collective over TP)
+mp_status tp_reduce_probe(mp_ctx* c, int b, int iters, double* seconds);
 // dE_r += dlogits^T Z over the first n_slots row blocks of b*s rows (one GEMM, K = n_slots b s)
 mp_status head_dE_deferred(mp_ctx* c, int b, int n_slots);
 

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 #include <vector>
@@ -132,6 +133,12 @@ static mp_status send(mp_ctx* c, bool act, const void* src, size_t bytes, cudaSt
   return MP_OK;
 }
 
+// slot -> destination copy on the consuming stream (16-byte vectors, grid sized to the SMs)
+__global__ void slot_copy_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, size_t n16) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
 static mp_status recv(mp_ctx* c, bool act, void* dst, size_t bytes, cudaStream_t st) {
   P2PRing& R = c->p2p;
   if (!R.slab || bytes > R.slot_bytes) return set_err(MP_ESTATE, "p2p ring not set up");
@@ -146,7 +153,15 @@ static mp_status recv(mp_ctx* c, bool act, void* dst, size_t bytes, cudaStream_t
   const char* src = (act ? act_ring(R.slab, R.slot_bytes) : grad_ring(R.slab, R.slot_bytes)) + (size_t)k * al(R.slot_bytes);
   unsigned wflags = CU_STREAM_WAIT_VALUE_GEQ | (R.flush_ok ? CU_STREAM_WAIT_VALUE_FLUSH : 0);
   MP_TRY(cu(g_wait((CUstream)st, (CUdeviceptr)(my_flags + ff), lap + 1, wflags), "wait full"));
-  MP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  if (bytes % 16 == 0 && ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
+    const size_t n16 = bytes / 16;
+    const int grid = (int)std::min<size_t>((n16 + 255) / 256, (size_t)num_sms() * 4);
+    slot_copy_kernel<<<grid, 256, 0, st>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst), n16);
+    count_launch();
+    MP_CUDA(cudaGetLastError());
+  } else {
+    MP_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+  }
   MP_TRY(cu(g_write((CUstream)st, (CUdeviceptr)(peer_flags + fe), lap + 1, CU_STREAM_WRITE_VALUE_DEFAULT),
             "write empty"));
   ++n;

@@ -11,8 +11,9 @@
 // operations, so no SM is held while a channel waits).  Every channel's send
 // order equals its receiver's consume order (checked by the oracle for every
 // schedule), so issuing receives in this rank's consume order cannot
-// deadlock and keeps the ideal bubble.  Compute waits on per-message events;
-// sends wait on the producing task's event.  After the flush the tied
+// deadlock and keeps the ideal bubble.  A receive runs on the compute stream
+// (wait for the slot's FULL flag, SM copy out of the slot, EMPTY flag), sends
+// on their channel streams after the producing task's event.  After the flush the tied
 // embedding gradient is all-reduced between the first and last stage and
 // one Adam step updates every parameter (strict optimizer semantics).
 #include <cuda_runtime.h>
@@ -511,11 +512,10 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
         x = local_act.at({tk.mb, sigma});
         local_act.erase({tk.mb, sigma});
       } else {
-        MP_TRY(alloc_async(c, &x, act_bytes, c->s_act_recv));
-        MP_TRY(p2p_recv_act(c, x, act_bytes, c->s_act_recv));
-        cudaEvent_t e = X.sync.get();
-        MP_CUDA(cudaEventRecord(e, c->s_act_recv));
-        MP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+        // received on the compute stream itself: it waits for the slot's FULL flag, copies the
+        // slot with an SM kernel and frees it (no channel-stream / event hop on the critical path)
+        MP_TRY(alloc_async(c, &x, act_bytes, cs));
+        MP_TRY(p2p_recv_act(c, x, act_bytes, cs));
       }
       cudaEvent_t t0 = X.timing.get(), t1 = X.timing.get();
       MP_CUDA(cudaEventRecord(t0, cs));
@@ -563,11 +563,8 @@ static mp_status run_batch_impl(mp_ctx* c, int B, int b, int m, mp_schedule sche
         dy = local_grad.at({tk.mb, sigma});
         local_grad.erase({tk.mb, sigma});
       } else {
-        MP_TRY(alloc_async(c, &dy, act_bytes, c->s_grad_recv));
-        MP_TRY(p2p_recv_grad(c, dy, act_bytes, c->s_grad_recv));
-        cudaEvent_t e = X.sync.get();
-        MP_CUDA(cudaEventRecord(e, c->s_grad_recv));
-        MP_CUDA(cudaStreamWaitEvent(cs, e, 0));
+        MP_TRY(alloc_async(c, &dy, act_bytes, cs));
+        MP_TRY(p2p_recv_grad(c, dy, act_bytes, cs));
       }
       cudaEvent_t t0 = X.timing.get(), t1 = X.timing.get();
       MP_CUDA(cudaEventRecord(t0, cs));
@@ -725,6 +722,13 @@ int mp_tp_comm_mode(const mp_ctx* c) {
   if (c->t == 1) return MP_TP_COMM_NCCL;
   if (!c->tps.tried) return MP_TP_COMM_AUTO;
   return c->tps.on ? MP_TP_COMM_NVLS : MP_TP_COMM_NCCL;
+}
+
+mp_status mp_tp_reduce_probe(mp_ctx* c, int b, int iters, double* seconds) {
+  if (!c || !seconds || b < 1 || iters < 1) return set_err(MP_EINVAL, "bad argument");
+  if (c->t == 1) return set_err(MP_EUNSUPPORTED, "tp probe: t = 1 has no tensor-parallel reduction");
+  MP_CUDA(cudaSetDevice(c->device));
+  return tp_reduce_probe(c, b, iters, seconds);
 }
 
 void* mp_compute_stream(mp_ctx* c) { return c ? reinterpret_cast<void*>(c->cs) : nullptr; }

@@ -93,6 +93,7 @@ SIGNATURES = {
     "mp_run_batch": (_I, [_P, _I, _I, _I, _I, _P, _I, ctypes.POINTER(_F), ctypes.POINTER(BatchStats)]),
     "mp_compute_stream": (_P, [_P]),
     "mp_tp_comm_mode": (_I, [_P]),
+    "mp_tp_reduce_probe": (_I, [_P, _I, _I, ctypes.POINTER(_D)]),
     "mp_run_batch_dev": (_I, [_P, _I, _I, _I, _I, _P, _I, _P, ctypes.POINTER(BatchStats)]),
     "mp_op_gemm": (_I, [_I, ctypes.POINTER(GemmDesc), _P]),
     "mp_gemm_flops": (_D, [ctypes.POINTER(GemmDesc)]),
@@ -284,6 +285,12 @@ class Context:
     def tp_comm_mode(self):
         """'nccl' / 'nvls' (the transport of the layer all-reduces), 'auto' before the first layer call."""
         return {v: k for k, v in TP_COMM.items()}[_sym("mp_tp_comm_mode")(self.ptr)]
+
+    def tp_reduce_probe(self, b, iters=20):
+        """Seconds per fused g / f reduction on the NVLS path (collective over the TP group)."""
+        sec = ctypes.c_double()
+        _check(_sym("mp_tp_reduce_probe")(self.ptr, b, iters, ctypes.byref(sec)))
+        return sec.value
 
     def run_batch_dev(self, B, b, m, sched, d_tokens, d_loss, apply_optimizer=False, stats=False):
         """Device-resident variant: d_tokens / d_loss are device addresses."""

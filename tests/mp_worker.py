@@ -122,6 +122,11 @@ def main():
             e = nw(ctx.get_grads(name, 0).reshape(r.shape), r)
             report["errors"][name] = e
             ok &= e < tol
+        if report["tp_comm"] == "nvls" and a.p == 1 and a.d == 1:
+            # the NVLink calibration entry point runs on the same symmetric buffers (collective)
+            sec = ctx.tp_reduce_probe(1, 3)
+            report["probe_us"] = sec * 1e6
+            ok &= sec > 0
         report["ok"] = bool(ok)
     finally:
         ctx.close()

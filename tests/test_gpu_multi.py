@@ -128,6 +128,8 @@ def test_multi_gpu_tp_transport(tmp_path, t, p, v, m, sched, tpcomm, dtype):
     assert r.returncode == 0, msg
     assert len(reps) == n and all(x["ok"] for x in reps), msg
     assert all(x.get("tp_comm") == tpcomm for x in reps), msg
+    if tpcomm == "nvls" and p == 1:
+        assert all(x.get("probe_us", 0) > 0 for x in reps), msg   # mp_tp_reduce_probe ran on every rank
 
 
 @pytest.mark.parametrize("dtype", ["bf16", "fp32"])
