@@ -277,12 +277,26 @@ def bubble_report(stats_list, world, p, v, m, sched, d=1):
             batches.append([vals])
     per_batch = [max(r[0] for r in pr) for pr in batches]
     med = float(np.median(per_batch))
+    # the paper's definition: a device idles from the batch start to its first
+    # task AND from its last task to the end of the whole pipeline, so the bubble of rank r is
+    # (global pipeline span - busy_r) / busy_r with the span = the longest rank's (all ranks
+    # start at a barrier); the per-rank-local value above stops at the rank's own last task
+    paper_mean, paper_max = [], []
+    for pr in batches:
+        span = max(r[1] for r in pr)
+        vals = [(span - r[2]) / r[2] for r in pr if r[2] > 0]
+        paper_mean.append(float(np.mean(vals)))
+        paper_max.append(float(np.max(vals)))
     mid = batches[int(np.argsort(per_batch)[len(per_batch) // 2])]
     per_rank = [[float(np.median([pr[r][k] for pr in batches])) for k in range(len(keys))]
                 for r in range(len(batches[0]))]
     st = stats_list[-1]
     rep = {"formula": st["bubble_formula"], "schedule": sched, "p": p, "v": v, "m": m,
            "batches": len(batches),
+           "paper_definition_mean_over_ranks": float(np.median(paper_mean)),
+           "paper_definition_max_over_ranks": float(np.median(paper_max)),
+           "paper_definition_rel_error_vs_formula": (float(np.median(paper_mean)) - st["bubble_formula"]) /
+           st["bubble_formula"] if st["bubble_formula"] else None,
            "measured_max_over_ranks": med,
            "measured_max_over_ranks_per_batch": [round(x, 5) for x in per_batch],
            "measured_per_rank_median_batch": [round(r[0], 5) for r in mid],
@@ -290,8 +304,10 @@ def bubble_report(stats_list, world, p, v, m, sched, d=1):
            "peak_inflight_rank0": st["peak_inflight"],
            "t_fwd_task_s": [round(r[3], 6) for r in per_rank], "t_bwd_task_s": [round(r[4], 6) for r in per_rank],
            "flush_and_optimizer_s": max(r[5] - r[1] for r in per_rank),
-           "how": "per-task CUDA events on the compute stream; bubble_r = (last task end - batch start - "
-                  "sum of task durations) / sum of task durations; max over ranks, median over batches"}
+           "how": "per-task CUDA events on the compute stream; measured_*: bubble_r = (last task end - batch "
+                  "start - sum of task durations) / sum of task durations (rank-local span), max over ranks; "
+                  "paper_definition_*: (longest rank's span - busy_r) / busy_r, i.e. warm-up AND cool-down "
+                  "idle of every rank (P:104-105), mean / max over ranks; medians over the batches"}
     if p > 1:
         # pipeline stage r = the ranks with pp = r in replica 0, rank = (dp p + pp) t + tp
         # (TP ranks of a stage behave alike: use the max)
