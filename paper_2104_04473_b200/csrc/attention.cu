@@ -361,6 +361,286 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
   if (warp == 1) tmem_dealloc<fa::TMEM_COLS>(tmem);
 }
 
+// ------------------------------------------------- forward, query-tile pairs
+// Two consecutive 128-row query tiles A = 2w, B = 2w + 1 of one head per CTA
+// (the K / V tiles are loaded once for both), with one softmax warpgroup per
+// tile so the tensor core and the two softmax groups ping-pong: while group A
+// turns S_A(j) into P_A(j), the MMA warp runs P_B(j-1) V and S_B(j), and the
+// other way round.  P is written back into TMEM over S (packed bf16) and read
+// from there as the A operand of O += P V, so no shared-memory P tiles exist.
+// Warps: 0 TMA, 1 MMA, 2-5 softmax A, 6-9 softmax B.
+// TMEM: S_A [0,128), S_B [128,256), O_A [256, 256+hd), O_B [384, 384+hd).
+// Same arithmetic as flash_fwd_kernel (lazy 2^8 rescaling, exp2, fp32 O).
+namespace fa2 {
+constexpr int THREADS = 320;
+constexpr int Q_BYTES = 2 * fa::BQ * 128;              // one Q tile (2 hd blocks of 64)
+constexpr int K_BYTES = 2 * fa::BKV * 128;
+constexpr int V_BYTES = 2 * 2 * 64 * 128;
+constexpr int SMEM = 2 * Q_BYTES + 2 * (K_BYTES + V_BYTES) + 1024 + 512;
+}  // namespace fa2
+
+template <bool DROP>
+__global__ void __launch_bounds__(fa2::THREADS, 1)
+flash_fwd_pair_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                      const __grid_constant__ CUtensorMap tmV, FaArgs g) {
+  using namespace fa;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;                                   // [2 tiles]
+  uint8_t* sK = sQ + 2 * fa2::Q_BYTES;                  // [2 stages]
+  uint8_t* sV = sK + 2 * fa2::K_BYTES;                  // [2 stages]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + 2 * fa2::V_BYTES);
+  uint64_t* q_full = bar + 0;
+  uint64_t* k_full = bar + 1;    // [2]
+  uint64_t* v_full = bar + 3;    // [2]
+  uint64_t* k_empty = bar + 5;   // [2] both S products of K(j) done
+  uint64_t* v_empty = bar + 7;   // [2] both P.V products of V(j) done
+  uint64_t* s_full = bar + 9;    // [2 tiles]
+  uint64_t* p_ready = bar + 11;  // [2 tiles] P written into TMEM (S read out)
+  uint64_t* pv_done = bar + 13;  // [2 tiles]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int npair = (g.nq + 1) / 2;
+  const int zn = (int)(gridDim.x / npair);
+  const int w = npair - 1 - (int)(blockIdx.x / zn);     // heaviest pairs first
+  const int z = (int)(blockIdx.x % zn);
+  const int qa = 2 * w, qb = 2 * w + 1;
+  const int nA = qa + 1, nB = qb < g.nq ? qb + 1 : 0;   // kv tiles per query tile (causal)
+  const int nkv = nB > 0 ? nB : nA;
+
+  if (threadIdx.x == 0) {
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&k_full[i], 1); mbar_init(&v_full[i], 1); mbar_init(&k_empty[i], 1); mbar_init(&v_empty[i], 1);
+      mbar_init(&s_full[i], 1); mbar_init(&p_ready[i], 128); mbar_init(&pv_done[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmQ); tma_prefetch(&tmK); tma_prefetch(&tmV); }
+  if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();   // the prologue above overlaps the previous kernel's tail
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ------------------------------------------------------- producer
+      const int ntile = nB > 0 ? 2 : 1;
+      mbar_arrive_expect_tx(q_full, ntile * g.nhb * BQ * 128);
+      for (int t = 0; t < ntile; ++t)
+        for (int hb = 0; hb < g.nhb; ++hb)
+          tma_load_3d(sQ + t * fa2::Q_BYTES + hb * BQ * 128, &tmQ, q_full, 64 * hb, (qa + t) * BQ, z);
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        if (j >= 2) mbar_wait(&k_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&k_full[st], g.nhb * BKV * 128);
+        for (int hb = 0; hb < g.nhb; ++hb)
+          tma_load_3d(sK + st * fa2::K_BYTES + hb * BKV * 128, &tmK, &k_full[st], 64 * hb, j * BKV, z);
+        if (j >= 2) mbar_wait(&v_empty[st], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&v_full[st], g.nhb * 2 * 64 * 128);
+        for (int hb = 0; hb < g.nhb; ++hb)
+          for (int kb = 0; kb < 2; ++kb)
+            tma_load_3d(sV + st * fa2::V_BYTES + hb * 2 * 8192 + kb * 8192, &tmV, &v_full[st], 64 * hb,
+                        j * BKV + 64 * kb, z);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ------------------------------------------------------ MMA issuer
+      // order: S_A(0) S_B(0) | PV_A(0) S_A(1) | PV_B(0) S_B(1) | PV_A(1) S_A(2) | ...
+      const uint32_t idesc_s = idesc_bf16(BQ, BKV, 0, 0);
+      const uint32_t idesc_o = idesc_bf16(BQ, g.hd, 0, 1);
+      const int ksteps_s = g.hd / 16;
+      mbar_wait(q_full, 0);
+      const uint32_t qbase = smem_u32(sQ);
+      auto issue_s = [&](int t, int j) {        // S_t = Q_t K_j^T into TMEM [128 t, +128)
+        const int st = j & 1;
+        const uint32_t qa_ = qbase + t * fa2::Q_BYTES, kb = smem_u32(sK + st * fa2::K_BYTES);
+        for (int k = 0; k < ksteps_s; ++k) {
+          const uint64_t ad = smem_desc_sw128(qa_ + (k / 4) * (BQ * 128) + (k % 4) * 32, 16, 1024);
+          const uint64_t bd = smem_desc_sw128(kb + (k / 4) * (BKV * 128) + (k % 4) * 32, 16, 1024);
+          umma_f16(tmem + 128 * t, ad, bd, idesc_s, k > 0 ? 1u : 0u);
+        }
+        umma_commit(&s_full[t]);
+      };
+      auto issue_pv = [&](int t, int j) {       // O_t += P_t V_j, P_t packed bf16 in TMEM [128 t, +64)
+        const int st = j & 1;
+        mbar_wait(&p_ready[t], j & 1);
+        tc_fence_after();
+        const uint32_t vb = smem_u32(sV + st * fa2::V_BYTES);
+#pragma unroll
+        for (int k = 0; k < BKV / 16; ++k) {
+          const uint64_t bd = smem_desc_sw128(vb + (k / 4) * 8192 + (k % 4) * 2048, 16384, 1024);
+          umma_f16_ts(tmem + 256 + 128 * t, tmem + 128 * t + 8 * k, bd, idesc_o, (j > 0 || k > 0) ? 1u : 0u);
+        }
+        umma_commit(&pv_done[t]);
+      };
+      for (int j = 0; j < nkv; ++j) {
+        const int st = j & 1;
+        const bool a_on = j < nA, b_on = j < nB;
+        mbar_wait(&k_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        if (j == 0) {
+          if (a_on) issue_s(0, 0);
+          if (b_on) issue_s(1, 0);
+        }
+        umma_commit(&k_empty[st]);   // (j > 0: S(j) of both tiles was issued in iteration j - 1)
+        mbar_wait(&v_full[st], (j >> 1) & 1);
+        tc_fence_after();
+        const bool next = j + 1 < nkv;
+        if (next) {                  // K(j+1) for the S products issued behind this tile's P.V
+          mbar_wait(&k_full[st ^ 1], ((j + 1) >> 1) & 1);
+          tc_fence_after();
+        }
+        if (a_on) {
+          issue_pv(0, j);
+          if (next && j + 1 < nA) issue_s(0, j + 1);
+        }
+        if (b_on) {
+          issue_pv(1, j);
+          if (next && j + 1 < nB) issue_s(1, j + 1);
+        }
+        umma_commit(&v_empty[st]);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- softmax
+    const int t = (warp - 2) / 4;                      // query tile of this warpgroup
+    const int nt = t == 0 ? nA : nB;
+    const int quarter = warp % 4;
+    const int r = quarter * 32 + lane;
+    const int qt = qa + t;
+    const int qrow = qt * BQ + r;
+    const uint32_t lane_off = (uint32_t)(quarter * 32) << 16;
+    const uint32_t scol = 128 * t, ocol = 256 + 128 * t;
+    float m = -FLT_MAX, l = 0.f;
+    const int zb = z / g.dp.heads, zj = z % g.dp.heads;
+    for (int j = 0; j < nt; ++j) {
+      mbar_wait(&s_full[t], j & 1);
+      tc_fence_after();
+      const bool diag = j == qt;
+      const int cut = diag ? r : 127;            // columns > cut are masked (causal diagonal tile)
+      // two passes over the S row in TMEM (32-column chunks, two loads in flight): the
+      // softmax state stays ~100 registers per thread, so both warpgroups fit the register
+      // file and alternate on the schedulers
+      float mxa[4] = {-FLT_MAX, -FLT_MAX, -FLT_MAX, -FLT_MAX};
+#pragma unroll
+      for (int c2 = 0; c2 < 4; c2 += 2) {
+        uint32_t va[32], vb[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + scol + 32 * c2, va);
+        tmem_ld_32x32b_x32(tmem + lane_off + scol + 32 * (c2 + 1), vb);
+        tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          if (32 * c2 + e <= cut) mxa[e & 3] = fmaxf(mxa[e & 3], __uint_as_float(va[e]));
+          if (32 * (c2 + 1) + e <= cut) mxa[e & 3] = fmaxf(mxa[e & 3], __uint_as_float(vb[e]));
+        }
+      }
+      const float mx = fmaxf(fmaxf(mxa[0], mxa[1]), fmaxf(mxa[2], mxa[3]));
+      const float mt = mx * g.scale_log2;
+      const bool need = __any_sync(0xffffffffu, mt > m + RESCALE_LOG2);
+      float alpha = 1.f;
+      if (need) {
+        const float m_new = fmaxf(m, mt);
+        alpha = ex2f(m - m_new);
+        m = m_new;
+        if (j > 0) {          // O holds P(0..j-1) V: wait for PV(j-1), then rescale it
+          mbar_wait(&pv_done[t], (j - 1) & 1);
+          tc_fence_after();
+          for (int c = 0; c < g.hd; c += 32) {
+            uint32_t o[32];
+            tmem_ld_32x32b_x32(tmem + lane_off + ocol + c, o);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
+            tmem_st_32x32b_x32(tmem + lane_off + ocol + c, o);
+          }
+        }
+      }
+      // P = exp2(s scale_log2 - m) -> packed bf16 pairs over S (chunks c2, c2+1 land in the
+      // columns of S chunk c2/2, already read); dropped entries zeroed, kept ones scaled, the
+      // row sum uses the undropped values
+      float rsa[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c2 = 0; c2 < 4; c2 += 2) {
+        uint32_t vv[2][32];
+        tmem_ld_32x32b_x32(tmem + lane_off + scol + 32 * c2, vv[0]);
+        tmem_ld_32x32b_x32(tmem + lane_off + scol + 32 * (c2 + 1), vv[1]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2) {
+          const int c = c2 + h2;
+          uint32_t km = 0xffffffffu;
+          if (DROP) {
+            km = 0;
+            const unsigned long long e0 = (unsigned long long)qrow * g.s + j * BKV + 32 * c;
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4)
+              km |= keep4(g.dp, e0 / 4 + q4, g.dp.head0 + zj, g.dp.seq0 + zb) << (4 * q4);
+          }
+          uint32_t wv[16];
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const int col = 32 * c + e;
+            float p0 = ex2f(fmaf(__uint_as_float(vv[h2][e]), g.scale_log2, -m));
+            float p1 = ex2f(fmaf(__uint_as_float(vv[h2][e + 1]), g.scale_log2, -m));
+            if (col > cut) p0 = 0.f;
+            if (col + 1 > cut) p1 = 0.f;
+            rsa[(e >> 1) & 3] += p0 + p1;
+            if (DROP) {
+              p0 = (km >> e) & 1 ? p0 * g.dp.scale : 0.f;
+              p1 = (km >> (e + 1)) & 1 ? p1 * g.dp.scale : 0.f;
+            }
+            __nv_bfloat162 pr = __floats2bfloat162_rn(p0, p1);
+            wv[e / 2] = *reinterpret_cast<uint32_t*>(&pr);
+          }
+          tmem_st_32x32b_x16(tmem + lane_off + scol + 16 * c, wv);
+        }
+      }
+      const float rs = (rsa[0] + rsa[1]) + (rsa[2] + rsa[3]);
+      l = l * alpha + rs;
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&p_ready[t]);
+    }
+    // epilogue: O / l -> bf16 context row, L2 = m + log2(l)
+    if (nt > 0) {
+      mbar_wait(&pv_done[t], (nt - 1) & 1);
+      tc_fence_after();
+      const float inv = 1.f / l;
+      const bool ok = qrow < g.s;
+      __nv_bfloat16* orow = g.O + (long long)qrow * g.ldo + (long long)z * g.hd;
+      for (int c = 0; c < g.hd; c += 32) {
+        uint32_t o[32];
+        tmem_ld_32x32b_x32(tmem + lane_off + ocol + c, o);
+        tmem_ld_wait();
+        if (ok) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 u;
+            uint32_t* wq = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              __nv_bfloat162 pr = __floats2bfloat162_rn(__uint_as_float(o[8 * q + 2 * e]) * inv,
+                                                        __uint_as_float(o[8 * q + 2 * e + 1]) * inv);
+              wq[e] = *reinterpret_cast<uint32_t*>(&pr);
+            }
+            *reinterpret_cast<uint4*>(orow + c + 8 * q) = u;
+          }
+        }
+      }
+      if (ok) g.L2[(long long)z * g.s + qrow] = m + log2f(l);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc<fa::TMEM_COLS>(tmem);
+}
+
 // ------------------------------------------------------------- backward
 // Per (head z, key/value tile j) CTA, looping over the query tiles i >= j:
 //   S = Q_i K_j^T, dP = dO_i V_j^T                       (TMEM [0,128), [128,256))
@@ -1017,6 +1297,30 @@ mp_status flash_attn_fwd(const void* QKV, void* O, float* L2, int s, int b, int 
     attr = true;
   }
   const FwdWork* work = (z < 65536 && a.nq < 65536) ? fwd_work((int)z, a.nq, hd) : nullptr;
+  // whole causal ranges: query-tile pairs (one K / V stream, two ping-ponging softmax groups)
+  // unless that leaves fewer than two CTAs per SM; MP_FA_FWD_PAIR=0 forces the single-tile kernel
+  const char* pe = getenv("MP_FA_FWD_PAIR");   // read per call (tests force both kernels)
+  const int pair_env = pe ? atoi(pe) : -1;
+  const long long pair_grid = z * ((a.nq + 1) / 2);
+  const bool pair = !work && pair_env != 0 && (pair_env == 1 || pair_grid >= 2LL * num_sms());
+  if (pair) {
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaError_t e = cudaFuncSetAttribute(flash_fwd_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           fa2::SMEM);
+      if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(flash_fwd_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, fa2::SMEM);
+      if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention smem attr: %s", cudaGetErrorString(e));
+      attr2 = true;
+    }
+    a.work = nullptr;
+    if (dp.on()) pdl_launch(flash_fwd_pair_kernel<true>, (unsigned)pair_grid, fa2::THREADS, fa2::SMEM, st, tq, tk, tv, a);
+    else pdl_launch(flash_fwd_pair_kernel<false>, (unsigned)pair_grid, fa2::THREADS, fa2::SMEM, st, tq, tk, tv, a);
+    count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(MP_ECUDA, "flash attention launch: %s", cudaGetErrorString(e));
+    return MP_OK;
+  }
   a.work = work ? work->dev : nullptr;
   a.Opart = work ? work->Opart : nullptr;
   a.ml = work ? work->ml : nullptr;

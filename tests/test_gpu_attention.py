@@ -12,9 +12,21 @@ from tests.gpu_util import dev, host, normwise
 pytestmark = pytest.mark.gpu
 
 
+# forward kernel: "auto" = the library's choice; "pair" forces the query-tile-pair forward
+# (two ping-ponging softmax warpgroups, P in TMEM), "single" the one-tile forward
+KERNELS = {"auto": None, "pair": "1", "single": "0"}
+
+
+@pytest.fixture(params=list(KERNELS))
+def fwd_kernel(request, monkeypatch):
+    if KERNELS[request.param] is not None:
+        monkeypatch.setenv("MP_FA_FWD_PAIR", KERNELS[request.param])
+    return request.param
+
+
 @pytest.mark.parametrize("s,b,heads,hd", [(128, 1, 1, 64), (256, 1, 2, 128), (384, 2, 3, 96), (200, 1, 2, 64),
                                           (2048, 1, 4, 128), (1000, 2, 2, 96), (32, 1, 2, 32), (640, 1, 2, 96)])
-def test_flash_fwd(s, b, heads, hd):
+def test_flash_fwd(s, b, heads, hd, fwd_kernel):
     QKV = gen.activations((s, b, heads, 3, hd), 41, 1.0, "bf16")
     q = dev(QKV.reshape(s, b, -1), "bf16")
     ctx = torch.zeros((s, b, heads * hd), dtype=torch.bfloat16, device="cuda")
@@ -37,7 +49,7 @@ def test_flash_fwd(s, b, heads, hd):
 
 @pytest.mark.parametrize("s,b,heads,hd", [(128, 1, 1, 64), (256, 1, 2, 128), (384, 2, 3, 96), (200, 1, 2, 64),
                                           (2048, 1, 2, 128), (1000, 2, 2, 96), (32, 1, 2, 32)])
-def test_flash_bwd(s, b, heads, hd):
+def test_flash_bwd(s, b, heads, hd, fwd_kernel):
     QKV = gen.activations((s, b, heads, 3, hd), 51, 1.0, "bf16")
     dC = gen.activations((s, b, heads * hd), 52, 1.0, "bf16")
     q = dev(QKV.reshape(s, b, -1), "bf16")
