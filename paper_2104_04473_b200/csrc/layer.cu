@@ -453,13 +453,19 @@ static mp_status tp_probe_t(mp_ctx* c, int b, int iters, double* seconds) {
     return bias_add_residual<T>((const T*)r, zb, zr, out, d.T, d.h, c->cs, Dropout{}, !two);
   };
   for (int i = 0; i < 3; ++i) MP_TRY(one());
-  cudaEvent_t e0 = c->events.at(0), e1 = c->events.at(1);
-  MP_CUDA(cudaEventRecord(e0, c->cs));
-  for (int i = 0; i < iters; ++i) MP_TRY(one());
-  MP_CUDA(cudaEventRecord(e1, c->cs));
-  MP_CUDA(cudaEventSynchronize(e1));
+  cudaEvent_t e0 = nullptr, e1 = nullptr;   // timing events (the context's own are sync-only)
+  MP_CUDA(cudaEventCreate(&e0));
+  MP_CUDA(cudaEventCreate(&e1));
+  mp_status s = MP_OK;
+  if (cudaEventRecord(e0, c->cs) != cudaSuccess) s = set_err(MP_ECUDA, "tp probe: event record");
+  for (int i = 0; i < iters && s == MP_OK; ++i) s = one();
   float ms = 0.f;
-  MP_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  if (s == MP_OK && (cudaEventRecord(e1, c->cs) != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess ||
+                     cudaEventElapsedTime(&ms, e0, e1) != cudaSuccess))
+    s = set_err(MP_ECUDA, "tp probe: event timing");
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  MP_TRY(s);
   *seconds = ms * 1e-3 / iters;
   MP_CUDA(cudaFreeAsync(blk, c->cs));
   return MP_OK;
