@@ -10,6 +10,8 @@ import sys
 
 import pytest
 
+import gen
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = pytest.mark.gpu
 
@@ -216,6 +218,15 @@ def test_multi_gpu_paper_width(tmp_path, t, p, v, m, sched):
     if ngpus() < n:
         pytest.skip(f"needs {n} GPUs")
     out = str(tmp_path / "rep")
+    # the fp64 oracle of the whole batch, computed here once with all host cores (inside the
+    # workers it would compete with the other ranks' processes for the CPU), read by every rank
+    import pickle
+    from oracle import model as M
+    shape = gen.ModelCfg(l=4, h=2304, a=24, s=2048, V=51200)
+    W = gen.model_weights(shape, seed=42, dtype="bf16")
+    tok = gen.tokens(m, shape.s, shape.V, seed=1234)
+    with open(out + ".oracle.pkl", "wb") as f:
+        pickle.dump(M.batch_fwd_bwd(W, tok, shape.a, m), f)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr=127.0.0.1", f"--master-port={free_port()}",
            os.path.join(ROOT, "tests", "mp_worker.py")]
