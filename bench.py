@@ -217,40 +217,17 @@ def run_reference(args, cfg, world, rank):
 
 
 def replay_bubble(p, m, v, sched, tf, tb):
-    """Ideal-pipeline replay of the library's own static task orders (mp_get_schedule)
-    with this run's measured per-rank mean task durations and zero communication:
-    the bubble the schedule itself implies once stage imbalance (embedding on the
-    first stage, logit layer + loss on the last) is accounted for.  Returns the
-    per-rank idle share (span_r - busy_r) / busy_r, span measured from t = 0."""
+    """Ideal-pipeline replay of the library's own static task orders with this run's
+    measured per-rank mean task durations and zero communication (mp_bubble_replay,
+    host-only C ABI): the bubble the schedule itself implies once stage imbalance
+    (embedding on the first stage, logit layer + loss on the last) is accounted for.
+    Returns the per-rank idle share (span_r - busy_r) / busy_r, span from t = 0, or
+    None if the replay cannot run."""
     from paper_2104_04473_b200 import mp
-    orders = [mp.mp_get_schedule(p, m, v, sched, r) for r in range(p)]
-    S = p * v
-    done, free, pos = {}, [0.0] * p, [0] * p
-    end = [0.0] * p
-    remaining = sum(len(o) for o in orders)
-    while remaining:
-        progressed = False
-        for r in range(p):
-            while pos[r] < len(orders[r]):
-                kind, i, c = orders[r][pos[r]]
-                sigma = c * p + r
-                if kind == "F":
-                    dep = None if sigma == 0 else ("F", i, sigma - 1)
-                else:
-                    dep = ("F", i, sigma) if sigma == S - 1 else ("B", i, sigma + 1)
-                if dep is not None and dep not in done:
-                    break
-                t0 = max(free[r], done[dep] if dep is not None else 0.0)
-                t1 = t0 + (tf[r] if kind == "F" else tb[r])
-                done[(kind, i, sigma)] = t1
-                free[r] = end[r] = t1
-                pos[r] += 1
-                remaining -= 1
-                progressed = True
-        if not progressed:
-            return None
-    busy = [m * v * (tf[r] + tb[r]) for r in range(p)]
-    return [(end[r] - busy[r]) / busy[r] for r in range(p)]
+    try:
+        return mp.mp_bubble_replay(p, m, v, sched, tf, tb)
+    except mp.MPError:
+        return None
 
 
 def bubble_report(stats_list, world, p, v, m, sched, d=1):

@@ -25,7 +25,7 @@
  *    NCCL communicators and internal streams; mp_finalize releases them.
  *  - There is no CPU fallback: compute calls fail with MP_ECUDA when no
  *    sm_100 device is present.  Host-only calls (mp_flops, mp_param_count,
- *    mp_get_schedule, mp_get_stage_map, mp_validate) need no GPU.
+ *    mp_get_schedule, mp_get_stage_map, mp_bubble_replay, mp_validate) need no GPU.
  */
 #ifndef MP_H_
 #define MP_H_
@@ -127,6 +127,18 @@ mp_status mp_get_schedule(int p, int m, int v, mp_schedule sched, int device, in
  * owns layers [sigma L_c, (sigma+1) L_c), L_c = l / (p v).  Output arrays
  * have l entries.  MP_EDIV if l % (p v) != 0. */
 mp_status mp_get_stage_map(int l, int p, int v, int* dev_of_layer, int* chunk_of_layer);
+/* Ideal-pipeline replay: the static task orders of
+ * mp_get_schedule executed with per-device forward / backward task durations
+ * tf[r], tb[r] (any unit, p entries each) and zero communication, every task
+ * starting when its device is free and its dependency (F(i, s-1); B(i, s+1) or
+ * F(i, S-1) on the last stage) has finished.  bubble[r] (p entries, caller-
+ * owned) = (end_r - busy_r) / busy_r with busy_r = m v (tf[r] + tb[r]) and
+ * end_r the device's last task end, t = 0 at the batch start: equal durations
+ * give exactly (p-1)/m (1F1B) or (p-1)/(v m) (interleaved) on device 0; unequal
+ * ones show what stage imbalance alone costs.  Host-only, no GPU.  MP_ESTATE if
+ * the orders deadlock (never for the library's schedules). */
+mp_status mp_bubble_replay(int p, int m, int v, mp_schedule sched, const double* tf, const double* tb,
+                           double* bubble);
 
 /* Thread-local description of the last error. */
 const char* mp_last_error(void);

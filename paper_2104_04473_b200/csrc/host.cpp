@@ -1,3 +1,4 @@
+#include <algorithm>
 // Host-only part of the C ABI: error state, Eq. (1)/(2), validation, the
 // schedule builder and the stage map.  No CUDA calls here (these entry points
 // work without a GPU), except the device query helpers at the bottom.
@@ -139,6 +140,51 @@ mp_status mp_get_schedule(int p, int m, int v, mp_schedule sched, int device, in
       triples[3 * i + 1] = tasks[i].mb;
       triples[3 * i + 2] = tasks[i].chunk;
     }
+  return MP_OK;
+}
+
+mp_status mp_bubble_replay(int p, int m, int v, mp_schedule sched, const double* tf, const double* tb,
+                           double* bubble) {
+  if (!tf || !tb || !bubble) return set_err(MP_EINVAL, "null argument");
+  if (p < 1 || m < 1 || v < 1) return set_err(MP_EINVAL, "p, m, v must be >= 1");
+  std::vector<std::vector<Task>> orders(p);
+  for (int r = 0; r < p; ++r) MP_TRY(build_schedule(p, m, v, sched, r, orders[r]));
+  const int S = p * v;
+  // end time of task (kind, microbatch, stage); < 0 = not yet run
+  std::vector<double> done(2 * (size_t)m * S, -1.0);
+  auto idx = [&](int kind, int mb, int sigma) { return ((size_t)kind * m + mb) * S + sigma; };
+  std::vector<double> free_at(p, 0.0);
+  std::vector<size_t> pos(p, 0);
+  size_t remaining = 0;
+  for (auto& o : orders) remaining += o.size();
+  while (remaining) {
+    bool progressed = false;
+    for (int r = 0; r < p; ++r) {
+      while (pos[r] < orders[r].size()) {
+        const Task& tk = orders[r][pos[r]];
+        const int sigma = tk.chunk * p + r;
+        double dep = 0.0;
+        if (tk.kind == 0) {                     // F(i, s) after F(i, s-1)
+          if (sigma > 0) dep = done[idx(0, tk.mb, sigma - 1)];
+        } else {                                // B(i, s) after B(i, s+1), or F(i, S-1) on the last stage
+          dep = sigma == S - 1 ? done[idx(0, tk.mb, sigma)] : done[idx(1, tk.mb, sigma + 1)];
+        }
+        if (dep < 0) break;
+        const double t0 = std::max(free_at[r], dep);
+        const double t1 = t0 + (tk.kind == 0 ? tf[r] : tb[r]);
+        done[idx(tk.kind, tk.mb, sigma)] = t1;
+        free_at[r] = t1;
+        ++pos[r];
+        --remaining;
+        progressed = true;
+      }
+    }
+    if (!progressed) return set_err(MP_ESTATE, "schedule replay deadlocked");
+  }
+  for (int r = 0; r < p; ++r) {
+    const double busy = (double)m * v * (tf[r] + tb[r]);
+    bubble[r] = busy > 0 ? (free_at[r] - busy) / busy : 0.0;
+  }
   return MP_OK;
 }
 

@@ -78,6 +78,7 @@ SIGNATURES = {
     "mp_validate": (_I, [ctypes.POINTER(ModelCfg), _I, _I, _I, _I, _I, _I, _I]),
     "mp_get_schedule": (_I, [_I, _I, _I, _I, _I, _P, ctypes.POINTER(_I)]),
     "mp_get_stage_map": (_I, [_I, _I, _I, _P, _P]),
+    "mp_bubble_replay": (_I, [_I, _I, _I, _I, _P, _P, _P]),
     "mp_last_error": (ctypes.c_char_p, []),
     "mp_nccl_id_bytes": (_I, []),
     "mp_nccl_get_id": (_I, [_P]),
@@ -184,6 +185,16 @@ def mp_get_stage_map(l, p, v):
     ch = (ctypes.c_int * l)()
     _check(_sym("mp_get_stage_map")(l, p, v, dev, ch))
     return list(dev), list(ch)
+
+
+def mp_bubble_replay(p, m, v, sched, tf, tb):
+    """Per-device idle share of the static task orders replayed with task durations
+    tf[r], tb[r] and zero communication (host-only, see include/mp.h)."""
+    a = (ctypes.c_double * p)(*tf)
+    b = (ctypes.c_double * p)(*tb)
+    out = (ctypes.c_double * p)()
+    _check(_sym("mp_bubble_replay")(p, m, v, SCHEDULES[sched], a, b, out))
+    return list(out)
 
 
 def mp_nccl_get_id():

@@ -92,3 +92,23 @@ def test_compute_call_without_gpu_fails_loudly():
     with pytest.raises(mp.MPError) as e:
         mp.mp_op_gemm("bf16", d)
     assert e.value.status == mp.MP_ECUDA
+
+
+@pytest.mark.parametrize("kind", ["gpipe", "1f1b", "interleaved"])
+@pytest.mark.parametrize("p,v", [(2, 1), (4, 1), (2, 2), (4, 2), (2, 3), (3, 2)])
+@pytest.mark.parametrize("tf,tb", [(1, 2), (3, 7)])
+def test_bubble_replay_matches_oracle_simulator(kind, p, v, tf, tb):
+    """mp_bubble_replay (the library's host-side replay the bench reports) against the
+    oracle's exact-rational event simulator of the same orders:
+    every device's idle share agrees, and device 0 attains the closed form."""
+    if kind != "interleaved" and v != 1:
+        pytest.skip("v > 1 only for the interleaved schedule")
+    for m in (p, 2 * p, 4 * p):
+        orders = SC.build_all(kind, p, m, v)
+        sim = SC.simulate(orders, p, v, tf, tb)
+        busy = m * (tf + tb)
+        ends = [max(e for (r, _), e in sim["end"].items() if r == dev) for dev in range(p)]
+        ref = [float((ends[r] - busy) / busy) for r in range(p)]
+        got = mp.mp_bubble_replay(p, m, v, kind, [tf / v] * p, [tb / v] * p)
+        assert max(abs(a - b) for a, b in zip(got, ref)) < 1e-12, (got, ref)
+        assert abs(got[0] - float(SC.bubble_formula(kind, p, m, v))) < 1e-12
