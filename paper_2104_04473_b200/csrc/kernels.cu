@@ -1,8 +1,11 @@
 // Memory-bound kernels of the hot path; see kernels.cuh for the contracts.
 // Design: every kernel streams 16-byte vectors (8 bf16 or 4 fp32) with the
 // thread index on the contiguous dimension, keeps one row in registers where
-// the op is a row reduction (LayerNorm: one CTA per row; causal softmax: one
-// warp per row), reduces with warp shuffles, and computes in fp32.
+// the op is a row reduction (LayerNorm forward: a group of threads per row,
+// several groups per persistent CTA; LayerNorm backward dx: one CTA per row;
+// causal softmax: one CTA per row), reduces with warp shuffles, and computes
+// in fp32.  Every kernel is launched with programmatic dependent launch
+// (launch.cuh) and starts with pdl_entry().
 #include "kernels.cuh"
 #include "common.h"
 #include "launch.cuh"
