@@ -174,6 +174,9 @@ mp_status mp_finalize(mp_ctx* ctx);
  * if this rank owns the layer (MP_OK and no-op otherwise).
  * Values are rounded to the storage dtype. */
 mp_status mp_set_weights(mp_ctx* ctx, const char* name, int layer, const float* host);
+/* Same with fp64 host data (e.g. the oracle's own arrays): each value is rounded once to
+ * fp32 (the master copy), then to the storage type, exactly as mp_set_weights would. */
+mp_status mp_set_weights_f64(mp_ctx* ctx, const char* name, int layer, const double* host);
 /* Read back this rank's shard of a weight / fp32 gradient accumulator into
  * host fp32 memory, in the shard's math orientation (e.g. W_qkv[:, cols of
  * this rank's heads]).  *n receives the element count; host may be NULL to

@@ -307,7 +307,10 @@ mp_status mp_finalize(mp_ctx* c) {
   return MP_OK;
 }
 
-mp_status mp_set_weights(mp_ctx* c, const char* name, int layer, const float* host) {
+}  // extern "C"
+
+template <class H>
+static mp_status set_weights_t(mp_ctx* c, const char* name, int layer, const H* host) {
   if (!c || !host) return set_err(MP_EINVAL, "null argument");
   int idx = -1; bool owned = false;
   MP_TRY(lookup(c, name, layer, &idx, &owned));
@@ -318,7 +321,7 @@ mp_status mp_set_weights(mp_ctx* c, const char* name, int layer, const float* ho
   std::vector<float> st((size_t)P.numel);
   for (int i = 0; i < sm.math_rows; ++i)
     for (int j = 0; j < sm.math_cols; ++j) {
-      const float val = host[full_index(c, P.name, i, j)];
+      const float val = (float)host[full_index(c, P.name, i, j)];   // fp64 input: rounded once
       if (sm.transposed) st[(size_t)j * sm.math_rows + i] = val;
       else st[(size_t)i * sm.math_cols + j] = val;
     }
@@ -327,6 +330,15 @@ mp_status mp_set_weights(mp_ctx* c, const char* name, int layer, const float* ho
   MP_TRY(cast_store(c, P.off, P.numel, c->cs));
   MP_CUDA(cudaStreamSynchronize(c->cs));
   return MP_OK;
+}
+
+extern "C" {
+
+mp_status mp_set_weights(mp_ctx* c, const char* name, int layer, const float* host) {
+  return set_weights_t(c, name, layer, host);
+}
+mp_status mp_set_weights_f64(mp_ctx* c, const char* name, int layer, const double* host) {
+  return set_weights_t(c, name, layer, host);
 }
 
 static mp_status get_common(mp_ctx* c, const char* name, int layer, float* host, long long* n, const float* base) {

@@ -85,6 +85,7 @@ SIGNATURES = {
     "mp_init": (_I, [_I, _I, _I, _I, ctypes.POINTER(ModelCfg), _I, _I, _I, _P, ctypes.POINTER(_P)]),
     "mp_finalize": (_I, [_P]),
     "mp_set_weights": (_I, [_P, ctypes.c_char_p, _I, _P]),
+    "mp_set_weights_f64": (_I, [_P, ctypes.c_char_p, _I, _P]),
     "mp_get_weights": (_I, [_P, ctypes.c_char_p, _I, _P, ctypes.POINTER(_LL)]),
     "mp_get_grads": (_I, [_P, ctypes.c_char_p, _I, _P, ctypes.POINTER(_LL)]),
     "mp_zero_grads": (_I, [_P]),

@@ -254,3 +254,23 @@ def test_run_batch_recompute(dtype, attn, h, pd):
     assert abs(res[1][0] - res[0][0]) <= 1e-6 * abs(res[0][0])
     assert stats["model_flops"] == float(F.flops(m, shape.s, shape.l, shape.h, shape.V, True))
     assert res[0][2]["model_flops"] == float(F.flops(m, shape.s, shape.l, shape.h, shape.V, False))
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+def test_set_weights_f64_matches_f32(dtype):
+    """mp_set_weights_f64 (fp64 host data, rounded once to fp32) stores exactly what
+    mp_set_weights stores for the same values rounded to fp32 on the host."""
+    shape = gen.TINY
+    W = gen.model_weights(shape, seed=7, dtype=dtype)
+    ctx = make_ctx(shape, dtype)
+    try:
+        for name, arr in W["layers"][0].items():
+            a64 = np.ascontiguousarray(arr, dtype=np.float64) * (1.0 + 1e-12)   # not representable in fp32
+            st = mp._sym("mp_set_weights_f64")(ctx.ptr, name.encode(), 0, a64.ctypes.data)
+            assert st == mp.MP_OK, mp.lib().mp_last_error()
+            got64 = ctx.get_weights(name, 0).copy()
+            ctx.set_weights(name, 0, a64.astype(np.float32))
+            got32 = ctx.get_weights(name, 0)
+            assert np.array_equal(got64, got32), name
+    finally:
+        ctx.close()
