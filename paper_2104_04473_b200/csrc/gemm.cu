@@ -7,9 +7,13 @@
 //   warp 1  : TMEM allocator + MMA issuer (one lane issues tcgen05.mma
 //             128 x BN x 16, fp32 accumulators in TMEM, double buffered so
 //             the epilogue of tile i overlaps the main loop of tile i+1);
-//   warps 2-5: epilogue, tcgen05.ld 32 columns per thread (one TMEM lane =
-//             one output row), + bias, convert, vectorised global stores or
-//             fp32 read-modify-write accumulation (weight gradients).
+//   warps 2-9: epilogue (two warps per TMEM lane quarter, alternate 128-byte
+//             column boxes), tcgen05.ld 32 columns per thread (one TMEM lane =
+//             one output row), + bias / GeLU / GeLU' / cross-entropy row
+//             statistics, convert, 128B-swizzled staging box -> TMA store, or
+//             TMA reduce-add into fp32 accumulators (weight gradients).
+// CTA pairs (cta_group::2) for large GEMMs; whole-tile waves + a stream-K tail
+// for accumulate GEMMs; raster by estimated DRAM traffic; launched with PDL.
 // Operands may be K-major or MN-major (the dX and dW GEMMs of the backward
 // and the P V / P^T dO attention products read MN-major tiles directly, so
 // no transpose is ever materialised -- the point of the paper's [s,b,a,h]
