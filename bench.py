@@ -230,6 +230,18 @@ def replay_bubble(p, m, v, sched, tf, tb):
         return None
 
 
+def paper_bubble(spans, busy):
+    """The paper's pipeline bubble of one batch from per-rank measurements:
+    every rank idles from the batch start to its first task and from its last task to
+    the end of the whole pipeline, so bubble_r = (max_r' span_r' - busy_r) / busy_r,
+    with span_r = the rank's last task end from the common batch start (all ranks start
+    at a barrier) and busy_r = its summed task durations.  Returns (mean, max) over the
+    ranks with busy_r > 0."""
+    total = max(spans)
+    vals = [(total - b) / b for b in busy if b > 0]
+    return float(np.mean(vals)), float(np.max(vals))
+
+
 def bubble_report(stats_list, world, p, v, m, sched, d=1):
     """Per-rank pipeline idle share (span_r - busy_r) / busy_r of each measured batch,
     max over ranks, median over the batches, next to the closed form (p-1)/m or
@@ -260,10 +272,9 @@ def bubble_report(stats_list, world, p, v, m, sched, d=1):
     # start at a barrier); the per-rank-local value above stops at the rank's own last task
     paper_mean, paper_max = [], []
     for pr in batches:
-        span = max(r[1] for r in pr)
-        vals = [(span - r[2]) / r[2] for r in pr if r[2] > 0]
-        paper_mean.append(float(np.mean(vals)))
-        paper_max.append(float(np.max(vals)))
+        mean_b, max_b = paper_bubble([r[1] for r in pr], [r[2] for r in pr])
+        paper_mean.append(mean_b)
+        paper_max.append(max_b)
     mid = batches[int(np.argsort(per_batch)[len(per_batch) // 2])]
     per_rank = [[float(np.median([pr[r][k] for pr in batches])) for k in range(len(keys))]
                 for r in range(len(batches[0]))]

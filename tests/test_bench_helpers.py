@@ -44,3 +44,27 @@ def test_workload_config_names_layout():
     c = bench.workload_config(a, gen.CONFIGS["1.7B"])
     assert c["parallelism"] == "t2p1v1d2" and c["m"] == 4 and c["d"] == 2 and c["recompute"]
     assert c["flop_formula"].startswith("Eq. (2) with recomputation")
+
+
+@pytest.mark.parametrize("p,m,v", [(2, 8, 1), (4, 8, 1), (4, 16, 2), (2, 8, 3)])
+def test_paper_bubble_of_an_ideal_pipeline_is_the_closed_form(p, m, v):
+    """Feeding bench.paper_bubble the per-device spans and busy times of an ideal
+    pipeline (the oracle's exact event simulation, equal stages) gives exactly
+    (p-1)/m or (p-1)/(v m) on every device: every device idles the
+    same total (p-1)(t_f+t_b)/v, split between warm-up and cool-down."""
+    from oracle import schedule as SC
+    kind = "interleaved" if v > 1 else "1f1b"
+    tf, tb = 1, 2
+    orders = SC.build_all(kind, p, m, v)
+    sim = SC.simulate(orders, p, v, tf, tb)
+    spans = [float(max(e for (r, _), e in sim["end"].items() if r == dev)) for dev in range(p)]
+    busy = [float(m * (tf + tb))] * p
+    mean_b, max_b = bench.paper_bubble(spans, busy)
+    f = (p - 1) / (v * m)
+    assert abs(mean_b - f) < 1e-12 and abs(max_b - f) < 1e-12
+
+
+def test_paper_bubble_counts_the_tail_idle():
+    # rank 1 ends early (its last task at 90 of a 100-long pipeline): its bubble includes the tail
+    mean_b, max_b = bench.paper_bubble([100.0, 90.0], [80.0, 80.0])
+    assert abs(max_b - 0.25) < 1e-12 and abs(mean_b - 0.25) < 1e-12
